@@ -1,0 +1,172 @@
+/*
+ * lfdg.h — C-ABI of the B200 (sm_100a) hot path of the superpixel light-field depth estimator
+ * (arXiv:1812.06856; reference: proj/include/lfd/*.hpp, a header-only C++20 CPU library).
+ *
+ * The reference has no FFI of its own: its hot path is the inline C++ API of
+ *   proj/include/lfd/superpixel.hpp:179  slic_segment
+ *   proj/include/lfd/sweep.hpp:112       sweep_view          (:141 plane_sweep_init)
+ *   proj/include/lfd/sweep.hpp:44        rasterize
+ *   proj/include/lfd/refine.hpp:53       make_refine_context
+ *   proj/include/lfd/refine.hpp:253      refine_iteration    (:325 run_refinement)
+ * and each entry point below names the one it replaces.  Everything is POD: plain pointers and
+ * sizes, no C++ or torch types, caller-allocated outputs, no exceptions across the boundary.
+ * Return codes map 1:1 onto the reference's exception classes (see LFDG_* below);
+ * lfdg_last_error() returns the message of the last failing call on the calling thread.
+ *
+ * State model.  A context owns one CUDA device and the device-resident copies of the
+ * reference's value types: the MultiViewSet (io.hpp:41: LAB images, cameras, DepthRange), one
+ * SuperpixelGrid per view (superpixel.hpp:39), one PlaneMap (sweep.hpp:27: planes + depth
+ * rasters) and, after lfdg_make_refine_context, the RefineContext tables (refine.hpp:40).
+ * Calls that take host pointers copy synchronously (the reference's call semantics); calls
+ * without host pointers only enqueue work on the context's stream (device-resident fast path).
+ * Results are bit-identical for any `workers` value in the reference, so there is none here.
+ */
+#ifndef LFDG_H
+#define LFDG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes --------------------------------------------------------------------- */
+#define LFDG_OK 0
+#define LFDG_INVALID_PARAMS 1 /* lfd::InvalidParams  (superpixel.hpp:14)                    */
+#define LFDG_INVARIANT 2      /* lfd::InvariantError (geometry.hpp:17)                      */
+#define LFDG_CUDA 3           /* CUDA runtime failure (std::runtime_error in the reference) */
+#define LFDG_STATE 4          /* call-order / index error (std::out_of_range analogue)      */
+
+/* ---- value types (layouts are part of the ABI) ---------------------------------------- */
+
+/* PinholeCamera (geometry.hpp:22): x_cam = R*X + t, pixel = dehom(K*x_cam); row-major. */
+typedef struct lfdg_camera {
+    double K[9];
+    double R[9];
+    double t[3];
+} lfdg_camera;
+
+/* SuperpixelRecord (superpixel.hpp:30), 40 bytes. */
+typedef struct lfdg_sp_record {
+    double cx, cy;
+    float mean_color[3];
+    int32_t pixel_count;
+    int32_t gx, gy;
+} lfdg_sp_record;
+
+/* SuperpixelPlane (geometry.hpp:65), 32 bytes: depth at the centroid + unit normal. */
+typedef struct lfdg_plane {
+    double depth;
+    double normal[3];
+} lfdg_plane;
+
+/* SlicParams (superpixel.hpp:18). Defaults: 12, 0.10f, 10. */
+typedef struct lfdg_slic_params {
+    int size;
+    float compactness;
+    int iterations;
+} lfdg_slic_params;
+
+/* SweepParams (sweep.hpp:14). Defaults: 80, 0.05f, 0. */
+typedef struct lfdg_sweep_params {
+    int levels;
+    float tssd_threshold;
+    int max_neighbors;
+} lfdg_sweep_params;
+
+/* EnergyParams (refine.hpp:15). Defaults: 0, 0.075f, 0.5f, 0, 5, 5, 0, 1, 1, 1. */
+typedef struct lfdg_energy_params {
+    double sigma;
+    float alpha;
+    float eta;
+    int size_init;
+    int steps_init;
+    int iterations;
+    int max_neighbors;
+    int use_smoothness;
+    int use_consistency;
+    int use_occlusion;
+} lfdg_energy_params;
+
+typedef struct lfdg_ctx lfdg_ctx;
+
+/* ---- context ---------------------------------------------------------------------------- */
+int lfdg_create(int device, lfdg_ctx** out);
+void lfdg_destroy(lfdg_ctx* ctx);
+const char* lfdg_last_error(void);
+/* Use an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream); NULL restores
+ * the context's own stream. */
+int lfdg_set_stream(lfdg_ctx* ctx, void* stream);
+int lfdg_synchronize(lfdg_ctx* ctx);
+/* Number of kernels this context has launched so far (for the bench's gpu_launches count). */
+uint64_t lfdg_launch_count(lfdg_ctx* ctx);
+
+/* ---- MultiViewSet (io.hpp:41) ------------------------------------------------------------ */
+/* images: [V][H][W][3] float scaled-LAB (image.hpp:83), host memory; cameras: [V]. Every view
+ * shares W x H (io.hpp:313-315).  Validates the DepthRange (geometry.hpp:57). */
+int lfdg_set_views(lfdg_ctx* ctx, int n_views, int width, int height, const float* images,
+                   const lfdg_camera* cameras, double d_min, double d_max);
+/* Re-upload the images of views [v0, v0+n) only (same shape as lfdg_set_views). */
+int lfdg_update_images(lfdg_ctx* ctx, int v0, int n, const float* images);
+
+/* ---- slic_segment (superpixel.hpp:179) --------------------------------------------------- */
+/* Segments view `view` of the context (its LAB image) and keeps the SuperpixelGrid resident. */
+int lfdg_slic_segment(lfdg_ctx* ctx, int view, const lfdg_slic_params* params);
+/* Segments views [v0, v0+n) in one batched pass (same result as n calls). */
+int lfdg_slic_segment_views(lfdg_ctx* ctx, int v0, int n, const lfdg_slic_params* params);
+int lfdg_grid_shape(lfdg_ctx* ctx, int view, int* grid_w, int* grid_h, int* cell_size);
+/* SuperpixelGrid → host: label_map [H*W], records [n], member CSR (grid.pixels) as
+ * offsets [n+1] + row-major member pixel indices [H*W].  Any pointer may be NULL. */
+int lfdg_get_grid(lfdg_ctx* ctx, int view, int32_t* label_map, lfdg_sp_record* records,
+                  int32_t* member_offsets, int32_t* member_pixels);
+/* grid_from_labels (pipeline.hpp:188): install a label map and recompute the statistics. */
+int lfdg_set_grid(lfdg_ctx* ctx, int view, int cell_size, const int32_t* label_map);
+
+/* ---- sweep_view / plane_sweep_init (sweep.hpp:112, :141) ---------------------------------- */
+/* Sweeps view `view` against matching_views (sweep.hpp:67); planes stay resident as the
+ * PlaneMap slot of that view; planes_out (NULL allowed) receives a host copy. */
+int lfdg_sweep_view(lfdg_ctx* ctx, int view, const lfdg_sweep_params* params, uint64_t seed,
+                    lfdg_plane* planes_out);
+int lfdg_sweep_views(lfdg_ctx* ctx, int v0, int n, const lfdg_sweep_params* params, uint64_t seed);
+/* matching_views (sweep.hpp:67): writes up to V-1 ids, returns the count in *n_out. */
+int lfdg_matching_views(lfdg_ctx* ctx, int view, int max_neighbors, int* out, int* n_out);
+
+/* ---- PlaneMap access / rasterize (sweep.hpp:27, :44) -------------------------------------- */
+int lfdg_set_planes(lfdg_ctx* ctx, int view, const lfdg_plane* planes);
+int lfdg_get_planes(lfdg_ctx* ctx, int view, lfdg_plane* planes);
+int lfdg_rasterize(lfdg_ctx* ctx);                     /* every view, like the reference */
+int lfdg_rasterize_views(lfdg_ctx* ctx, int v0, int n);
+int lfdg_get_depth(lfdg_ctx* ctx, int view, float* depth);
+int lfdg_set_depth(lfdg_ctx* ctx, int view, const float* depth);
+
+/* ---- refinement (refine.hpp:53, :253, :325) ----------------------------------------------- */
+/* make_refine_context: resolves sigma (0 → 1.5·inverse_depth_step) and size_init (0 → min(W,H))
+ * exactly as refine.hpp:56-57 and builds the static tables on the device. */
+int lfdg_make_refine_context(lfdg_ctx* ctx, const lfdg_energy_params* params, int sweep_levels,
+                             double* sigma_out, int* size_init_out);
+/* Refine only views [v0, v0+n) (the multi-GPU view partition); default is every view. */
+int lfdg_set_refine_views(lfdg_ctx* ctx, int v0, int n);
+/* refine_iteration(ctx, state, l): the PlaneMap planes of the refined views are replaced by the
+ * Jacobi update computed from the current planes + depth rasters (the caller rasterizes, as
+ * run_refinement does).  accepted/violations (NULL allowed) receive RefineStats (refine.hpp:244)
+ * counters; violations is always 0 here because acceptance is strict by construction. */
+int lfdg_refine_iteration(lfdg_ctx* ctx, int l, uint64_t* accepted, uint64_t* violations);
+/* run_refinement: l = 1..iterations of (refine_iteration; rasterize). */
+int lfdg_run_refinement(lfdg_ctx* ctx, uint64_t* accepted, uint64_t* violations);
+/* min_neighbor_similarity table of make_refine_context (refine.hpp:71), [nsp] floats. */
+int lfdg_get_min_nb_sim(lfdg_ctx* ctx, int view, float* out);
+
+/* ---- device buffers (multi-GPU all-gather plumbing) --------------------------------------- */
+/* Raw device pointer + byte size of one all-view buffer, laid out [V][per-view block]:
+ * 0 labels i32[H*W], 1 records (SoA block), 2 member offsets i32[nsp+1],
+ * 3 member pixels i32[H*W], 4 planes f64x4[nsp], 5 depth f32[H*W].  *view_stride is the
+ * per-view block size in bytes. */
+int lfdg_device_buffer(lfdg_ctx* ctx, int which, void** ptr, size_t* bytes, size_t* view_stride);
+/* After an external all-gather filled buffers of views this context did not compute. */
+int lfdg_mark_views_ready(lfdg_ctx* ctx, int v0, int n, int what);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LFDG_H */

@@ -1,0 +1,134 @@
+// Host-side context: device-resident copies of the reference's value types.
+//
+// HBM layout (all views of one context share W x H and the superpixel cell size S):
+//   lab      float4 [V][H*W]   scaled-LAB image (image.hpp:83), w = 0 pad -> one 16 B load
+//   labels   int32  [V][H*W]   SuperpixelGrid::label_map (superpixel.hpp:43)
+//   cx, cy   f64    [V][nsp]   SuperpixelRecord centroid (superpixel.hpp:31)
+//   color    float4 [V][nsp]   SuperpixelRecord::mean_color
+//   count    int32  [V][nsp]   SuperpixelRecord::pixel_count
+//   moff     int32  [V][nsp+1] CSR offsets of SuperpixelGrid::pixels
+//   mpix     int32  [V][H*W]   CSR member pixel indices, row-major per superpixel
+//   planes   f64x4  [V][nsp]   PlaneMap::planes {depth, nx, ny, nz} (sweep.hpp:28)
+//   depth    f32    [V][H*W]   PlaneMap::depth (sweep.hpp:29)
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/lfdg.h"
+#include "common.cuh"
+
+namespace lfdg {
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define LFDG_CUDA_CHECK(expr)                                                                      \
+    do {                                                                                           \
+        cudaError_t e_ = (expr);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            throw ::lfdg::Error(LFDG_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));    \
+    } while (0)
+
+// Kernel launch bookkeeping: checks the launch and counts it.
+#define LFDG_LAUNCHED(ctx)                          \
+    do {                                            \
+        LFDG_CUDA_CHECK(cudaGetLastError());        \
+        (ctx)->launches++;                          \
+    } while (0)
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void alloc(size_t count) {
+        if (count == n && p) return;
+        release();
+        if (count) LFDG_CUDA_CHECK(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~DevBuf() { release(); }
+};
+
+// Static tables of make_refine_context (refine.hpp:53-79) on the device.
+struct RefineTables {
+    bool ready = false;
+    lfdg_energy_params params{};  // sigma / size_init resolved
+    int n_targets = 0;
+    std::vector<int> targets_host;  // [V][n_targets]
+    DevBuf<int> targets;            // [V][n_targets]
+    DevBuf<double> rel;             // [V][n_targets][12]: rel_rot (9, row-major) + rel_trans (3)
+    DevBuf<float> min_nb_sim;       // [V][nsp]
+    DevBuf<float> ring_w;           // [V][nsp][8] color_similarity to ring neighbour k (or -1: absent)
+};
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    uint64_t launches = 0;
+    int sm_count = 148;
+
+    // MultiViewSet
+    int V = 0, W = 0, H = 0;
+    double d_min = 0, d_max = 0;
+    std::vector<lfdg_camera> cams;
+    bool identity_rot = false;   // every R is exactly I
+    bool canonical_k = false;    // every K has K01 = K10 = K20 = K21 = 0, K22 = 1
+    DevBuf<Cam> d_cams;
+    DevBuf<float4> lab;
+
+    // SuperpixelGrid (uniform S over views)
+    int S = 0, gw = 0, gh = 0, nsp = 0;
+    std::vector<char> grid_ready;
+    DevBuf<int32_t> labels, moff, mpix, count;
+    DevBuf<double> cx, cy;
+    DevBuf<float4> color;
+    DevBuf<double2> cray;  // [V][nsp] ray through the centroid (geometry.hpp:45), for rasterize
+
+    // PlaneMap
+    std::vector<char> planes_ready;
+    DevBuf<double4> planes, planes_next;
+    DevBuf<float> depth;
+
+    // refinement
+    RefineTables refine;
+    int refine_v0 = 0, refine_n = -1;  // -1: all views
+    DevBuf<unsigned long long> counters;  // [2]: accepted, violations
+
+    size_t hw() const { return static_cast<size_t>(W) * H; }
+    void require_views() const {
+        if (V <= 0) throw Error(LFDG_STATE, "no views: call lfdg_set_views first");
+    }
+    void require_view(int v) const {
+        require_views();
+        if (v < 0 || v >= V) throw Error(LFDG_STATE, "view index out of range");
+    }
+    void require_grid(int v) const {
+        require_view(v);
+        if (!grid_ready[v]) throw Error(LFDG_STATE, "view has no superpixel grid: segment it first");
+    }
+};
+
+// ---- stage entry points (implemented in the .cu files) ----------------------------------
+void ensure_grid_buffers(Ctx& c, int S);
+void slic_views(Ctx& c, int v0, int n, const lfdg_slic_params& p);          // slic.cu
+void grid_from_labels(Ctx& c, int v, int S, const int32_t* host_labels);     // slic.cu
+void sweep_views(Ctx& c, int v0, int n, const lfdg_sweep_params& p, uint64_t seed);  // sweep.cu
+void rasterize_views(Ctx& c, int v0, int n);                                   // sweep.cu
+std::vector<int> matching_views(const Ctx& c, int view, int max_neighbors);    // sweep.cu
+void make_refine_tables(Ctx& c, const lfdg_energy_params& p, int sweep_levels);  // refine.cu
+void refine_iteration(Ctx& c, int l);                                            // refine.cu
+
+}  // namespace lfdg

@@ -1,0 +1,318 @@
+// Plane-sweep initialisation and rasterization on sm_100a.
+//
+//   k_sweep      sweep_view (sweep.hpp:112-139) + sweep_cost (sweep.hpp:85-107): one CTA per
+//                (view, superpixel), one thread per depth hypothesis.  Member rays and reference
+//                colours are staged once in shared memory; each thread accumulates its own FP64
+//                cost in exactly the reference's (target, member-pixel) order, so costs are
+//                bit-identical; the (cost, depth) argmin is a block reduction on a total order,
+//                which reproduces "ties -> smaller depth" (sweep.hpp:130).
+//   k_rasterize  rasterize (sweep.hpp:44-63): one thread per pixel.
+//
+// FP64 geometry follows geometry.hpp:70-111 operation by operation.  Two template switches
+// drop operations that are exact identities for the camera set at hand (checked on the host,
+// DESIGN.md "sweep"): kIdR when every rotation is exactly I (then R^T a = a and R w = w up to
+// the sign of a zero, which cannot reach the cost: contains() treats -0 as 0 and the bilinear
+// residual is squared), kCanonK when every K has K01 = K10 = K20 = K21 = 0 and K22 = 1 (then
+// h.z = z whenever z > 0, which is the only case that is sampled).
+#include <algorithm>
+#include <cmath>
+
+#include "context.h"
+
+namespace lfdg {
+namespace {
+
+constexpr int kSweepCap = 1024;  // member pixels staged per chunk
+
+template <bool kIdR, bool kCanonK>
+__device__ __forceinline__ float sweep_sample(const Cam& rc, const Cam& tc, const float4* __restrict__ timg, int W,
+                                              int H, double d, double vx, double vy, float4 ref, float T) {
+    // backproject (geometry.hpp:70-73): world = R^T (d * ray - t)
+    const double a0 = d * vx - rc.t[0];
+    const double a1 = d * vy - rc.t[1];
+    const double a2 = d - rc.t[2];
+    double w0, w1, w2;
+    if (kIdR) {
+        w0 = a0;
+        w1 = a1;
+        w2 = a2;
+    } else {
+        w0 = (rc.R[0] * a0 + rc.R[3] * a1) + rc.R[6] * a2;
+        w1 = (rc.R[1] * a0 + rc.R[4] * a1) + rc.R[7] * a2;
+        w2 = (rc.R[2] * a0 + rc.R[5] * a1) + rc.R[8] * a2;
+    }
+    // project (geometry.hpp:76-80): x = R X + t, h = K x
+    double c0, c1, c2;
+    if (kIdR) {
+        c0 = w0 + tc.t[0];
+        c1 = w1 + tc.t[1];
+        c2 = w2 + tc.t[2];
+    } else {
+        c0 = ((tc.R[0] * w0 + tc.R[1] * w1) + tc.R[2] * w2) + tc.t[0];
+        c1 = ((tc.R[3] * w0 + tc.R[4] * w1) + tc.R[5] * w2) + tc.t[1];
+        c2 = ((tc.R[6] * w0 + tc.R[7] * w1) + tc.R[8] * w2) + tc.t[2];
+    }
+    if (c2 <= 0) return T;  // behind the target camera (geometry.hpp:109)
+    double hx, hy, hz;
+    if (kCanonK) {
+        hx = tc.K[0] * c0 + tc.K[2] * c2;
+        hy = tc.K[4] * c1 + tc.K[5] * c2;
+        hz = c2;
+    } else {
+        hx = (tc.K[0] * c0 + tc.K[1] * c1) + tc.K[2] * c2;
+        hy = (tc.K[3] * c0 + tc.K[4] * c1) + tc.K[5] * c2;
+        hz = (tc.K[6] * c0 + tc.K[7] * c1) + tc.K[8] * c2;
+    }
+    const double u = hx / hz;
+    const double v = hy / hz;
+    // ImageBuffer::contains (image.hpp:42-44)
+    if (!(u >= 0.0 && v >= 0.0 && u <= W - 1.0 && v <= H - 1.0)) return T;
+    // ImageBuffer::bilinear (image.hpp:47-67)
+    int x0 = (int)floor(u);
+    int y0 = (int)floor(v);
+    if (x0 >= W - 1) x0 = W - 2;
+    if (y0 >= H - 1) y0 = H - 2;
+    if (x0 < 0) x0 = 0;
+    if (y0 < 0) y0 = 0;
+    const float fx = (float)(u - x0);
+    const float fy = (float)(v - y0);
+    const float4* r0 = timg + (size_t)y0 * W + x0;
+    const float4 p00 = __ldg(r0), p10 = __ldg(r0 + 1);
+    const float4 p01 = __ldg(r0 + W), p11 = __ldg(r0 + W + 1);
+    float o0, o1, o2;
+    {
+        const float top = p00.x + fx * (p10.x - p00.x);
+        const float bot = p01.x + fx * (p11.x - p01.x);
+        o0 = top + fy * (bot - top);
+    }
+    {
+        const float top = p00.y + fx * (p10.y - p00.y);
+        const float bot = p01.y + fx * (p11.y - p01.y);
+        o1 = top + fy * (bot - top);
+    }
+    {
+        const float top = p00.z + fx * (p10.z - p00.z);
+        const float bot = p01.z + fx * (p11.z - p01.z);
+        o2 = top + fy * (bot - top);
+    }
+    // tssd (sweep.hpp:32-34): std::min(T, dist2)
+    const float d2 = color_dist2(ref.x, ref.y, ref.z, o0, o1, o2);
+    return d2 < T ? d2 : T;
+}
+
+template <bool kIdR, bool kCanonK>
+__global__ void __launch_bounds__(256) k_sweep(const float4* __restrict__ lab, int W, int H, int nsp, int v0,
+                                               const Cam* __restrict__ cams, const int* __restrict__ targets,
+                                               int n_targets, const int32_t* __restrict__ moff,
+                                               const int32_t* __restrict__ mpix, int levels, double inv_lo,
+                                               double inv_hi, double step, float T, uint64_t seed,
+                                               double4* planes) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double2* s_ray = reinterpret_cast<double2*>(smem);
+    float4* s_ref = reinterpret_cast<float4*>(smem + kSweepCap * sizeof(double2));
+    Cam* s_cam = reinterpret_cast<Cam*>(smem + kSweepCap * (sizeof(double2) + sizeof(float4)));
+    __shared__ double red_c[32];
+    __shared__ double red_d[32];
+
+    const int sp = blockIdx.x;
+    const int view = v0 + blockIdx.y;
+    const size_t hw = (size_t)W * H;
+    const int* tg = targets + (size_t)view * n_targets;
+    for (int i = threadIdx.x; i < n_targets + 1; i += blockDim.x) s_cam[i] = cams[i == 0 ? view : tg[i - 1]];
+    const int32_t m0 = moff[(size_t)view * (nsp + 1) + sp];
+    const int n = moff[(size_t)view * (nsp + 1) + sp + 1] - m0;
+    const int32_t* mem = mpix + (size_t)view * hw + m0;
+    const float4* rimg = lab + (size_t)view * hw;
+    __syncthreads();
+    const Cam& rc = s_cam[0];
+
+    auto load_chunk = [&](int c0) {
+        const int cn = min(kSweepCap, n - c0);
+        for (int i = threadIdx.x; i < cn; i += blockDim.x) {
+            const int p = mem[c0 + i];
+            const int x = p % W, y = p / W;
+            double rx, ry;
+            cam_ray(rc, (double)x, (double)y, rx, ry);
+            s_ray[i] = make_double2(rx, ry);
+            s_ref[i] = rimg[p];
+        }
+    };
+
+    const uint64_t s0 = derive_stream_state(seed, (uint64_t)view, (uint64_t)sp);
+    // Hypotheses of this thread: k = threadIdx.x, + blockDim.x, ...  (uniform trip count so the
+    // block-wide chunk loads below stay convergent).
+    const int per = (levels + blockDim.x - 1) / blockDim.x;
+    double best_c = 0, best_d = 0;
+    bool have = false;
+    for (int r = 0; r < per; ++r) {
+        const int k = r * blockDim.x + threadIdx.x;
+        const bool active = k < levels;
+        double d = 0;
+        if (active) {
+            // sample_inverse_depths (geometry.hpp:116-130)
+            double inv = inv_lo + step * k + u64_to_unit(splitmix_at(s0, (uint64_t)k)) * step;
+            if (inv > inv_hi) inv = inv_hi;
+            d = 1.0 / inv;
+        }
+        double cost = 0;
+        for (int ti = 0; ti < n_targets; ++ti) {
+            const Cam& tc = s_cam[ti + 1];
+            const float4* timg = lab + (size_t)tg[ti] * hw;
+            for (int c0 = 0; c0 < n; c0 += kSweepCap) {
+                if (n > kSweepCap || (ti == 0 && c0 == 0 && r == 0)) {
+                    __syncthreads();
+                    load_chunk(c0);
+                    __syncthreads();
+                }
+                if (!active) continue;
+                const int cn = min(kSweepCap, n - c0);
+                for (int i = 0; i < cn; ++i) {
+                    const double2 ray = s_ray[i];
+                    const float t = sweep_sample<kIdR, kCanonK>(rc, tc, timg, W, H, d, ray.x, ray.y, s_ref[i], T);
+                    cost += (double)t;
+                }
+            }
+        }
+        if (active && (!have || cost < best_c || (cost == best_c && d < best_d))) {
+            best_c = cost;
+            best_d = d;
+            have = true;
+        }
+    }
+    if (!have) {
+        best_c = INFINITY;
+        best_d = INFINITY;
+    }
+    // block argmin on (cost, depth)
+    for (int off = 16; off; off >>= 1) {
+        const double oc = __shfl_xor_sync(LFDG_FULL_MASK, best_c, off);
+        const double od = __shfl_xor_sync(LFDG_FULL_MASK, best_d, off);
+        if (oc < best_c || (oc == best_c && od < best_d)) {
+            best_c = oc;
+            best_d = od;
+        }
+    }
+    const int warp = threadIdx.x >> 5, nwarps = (blockDim.x + 31) >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        red_c[warp] = best_c;
+        red_d[warp] = best_d;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double bc = red_c[0], bd = red_d[0];
+        for (int w = 1; w < nwarps; ++w)
+            if (red_c[w] < bc || (red_c[w] == bc && red_d[w] < bd)) {
+                bc = red_c[w];
+                bd = red_d[w];
+            }
+        planes[(size_t)view * nsp + sp] = make_double4(bd, 0.0, 0.0, -1.0);
+    }
+}
+
+// rasterize (sweep.hpp:44-63), one thread per pixel of views [v0, v0+n).
+__global__ void k_rasterize(const int32_t* __restrict__ labels, const double4* __restrict__ planes,
+                            const double2* __restrict__ cray, const Cam* __restrict__ cams, int W, int H, int nsp,
+                            int v0, float* depth) {
+    const size_t hw = (size_t)W * H;
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= hw) return;
+    const int v = v0 + blockIdx.y;
+    const int l = labels[(size_t)v * hw + i];
+    const double4 pl = planes[(size_t)v * nsp + l];
+    const double2 cr = cray[(size_t)v * nsp + l];
+    const double ax = pl.x * cr.x, ay = pl.x * cr.y, az = pl.x;
+    const double num = (pl.y * ax + pl.z * ay) + pl.w * az;
+    const int x = (int)(i % W), y = (int)(i / W);
+    double rx, ry;
+    cam_ray(cams[v], (double)x, (double)y, rx, ry);
+    const double denom = (pl.y * rx + pl.z * ry) + pl.w;
+    depth[(size_t)v * hw + i] = fabs(denom) <= 1e-9 ? 0.f : (float)(num / denom);
+}
+
+inline unsigned ceil_div(size_t a, size_t b) { return (unsigned)((a + b - 1) / b); }
+
+}  // namespace
+
+// matching_views (sweep.hpp:67-80), on the host with Eigen's operation order.
+std::vector<int> matching_views(const Ctx& c, int view, int max_neighbors) {
+    std::vector<int> others;
+    for (int i = 0; i < c.V; ++i)
+        if (i != view) others.push_back(i);
+    if (max_neighbors > 0 && static_cast<int>(others.size()) > max_neighbors) {
+        auto center = [&](int v, double out[3]) {
+            const lfdg_camera& k = c.cams[v];
+            for (int i = 0; i < 3; ++i)
+                out[i] = ((-k.R[0 * 3 + i]) * k.t[0] + (-k.R[1 * 3 + i]) * k.t[1]) + (-k.R[2 * 3 + i]) * k.t[2];
+        };
+        double cv[3];
+        center(view, cv);
+        auto d2 = [&](int v) {
+            double cc[3];
+            center(v, cc);
+            const double a = cc[0] - cv[0], b = cc[1] - cv[1], e = cc[2] - cv[2];
+            return (a * a + b * b) + e * e;
+        };
+        std::stable_sort(others.begin(), others.end(), [&](int a, int b) { return d2(a) < d2(b); });
+        others.resize(max_neighbors);
+        std::sort(others.begin(), others.end());
+    }
+    return others;
+}
+
+void sweep_views(Ctx& c, int v0, int n, const lfdg_sweep_params& p, uint64_t seed) {
+    if (p.levels < 2) throw Error(LFDG_INVALID_PARAMS, "sweep levels must be >= 2");
+    if (!(p.tssd_threshold > 0)) throw Error(LFDG_INVALID_PARAMS, "tssd threshold must be > 0");
+    if (!(0 < c.d_min && c.d_min < c.d_max)) throw Error(LFDG_INVARIANT, "depth range requires 0 < d_min < d_max");
+    if (v0 < 0 || n < 0 || v0 + n > c.V) throw Error(LFDG_STATE, "view range out of bounds");
+    for (int v = 0; v < c.V; ++v) c.require_grid(v);  // sweep_cost reads only the own grid, but
+    // matching_views needs V and the rasterize that follows needs every grid.
+    if (n == 0) return;
+    const int nt = c.V - 1 > 0 && p.max_neighbors > 0 ? std::min(p.max_neighbors, c.V - 1) : c.V - 1;
+    std::vector<int> tg((size_t)c.V * std::max(nt, 1), 0);
+    for (int v = 0; v < c.V; ++v) {
+        const std::vector<int> t = matching_views(c, v, p.max_neighbors);
+        for (int i = 0; i < nt; ++i) tg[(size_t)v * nt + i] = t[i];
+    }
+    DevBuf<int> d_tg;
+    d_tg.alloc(tg.size());
+    LFDG_CUDA_CHECK(cudaMemcpyAsync(d_tg.p, tg.data(), tg.size() * sizeof(int), cudaMemcpyHostToDevice, c.stream));
+    const double inv_lo = 1.0 / c.d_max;
+    const double inv_hi = 1.0 / c.d_min;
+    const double step = (inv_hi - inv_lo) / (p.levels - 1);
+    const int threads = std::min(256, (p.levels + 31) / 32 * 32);
+    const size_t smem = kSweepCap * (sizeof(double2) + sizeof(float4)) + (size_t)(nt + 1) * sizeof(Cam);
+    dim3 grid(c.nsp, n);
+    auto launch = [&](auto kernel) {
+        LFDG_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kernel<<<grid, threads, smem, c.stream>>>(c.lab.p, c.W, c.H, c.nsp, v0, c.d_cams.p, d_tg.p, nt, c.moff.p,
+                                                  c.mpix.p, p.levels, inv_lo, inv_hi, step, p.tssd_threshold, seed,
+                                                  c.planes.p);
+    };
+    if (c.identity_rot && c.canonical_k)
+        launch(k_sweep<true, true>);
+    else if (c.identity_rot)
+        launch(k_sweep<true, false>);
+    else if (c.canonical_k)
+        launch(k_sweep<false, true>);
+    else
+        launch(k_sweep<false, false>);
+    LFDG_LAUNCHED(&c);
+    // d_tg is freed at scope exit; make sure the kernel has consumed it.
+    LFDG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    for (int b = 0; b < n; ++b) c.planes_ready[v0 + b] = 1;
+}
+
+void rasterize_views(Ctx& c, int v0, int n) {
+    if (v0 < 0 || n < 0 || v0 + n > c.V) throw Error(LFDG_STATE, "view range out of bounds");
+    for (int v = v0; v < v0 + n; ++v) {
+        c.require_grid(v);
+        if (!c.planes_ready[v]) throw Error(LFDG_STATE, "view has no planes: sweep or set them first");
+    }
+    if (n == 0) return;
+    if (!c.depth.p) c.depth.alloc((size_t)c.V * c.hw());
+    k_rasterize<<<dim3(ceil_div(c.hw(), 256), n), 256, 0, c.stream>>>(c.labels.p, c.planes.p, c.cray.p, c.d_cams.p,
+                                                                      c.W, c.H, c.nsp, v0, c.depth.p);
+    LFDG_LAUNCHED(&c);
+}
+
+}  // namespace lfdg
