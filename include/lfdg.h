@@ -159,12 +159,18 @@ int lfdg_get_min_nb_sim(lfdg_ctx* ctx, int view, float* out);
 
 /* ---- device buffers (multi-GPU all-gather plumbing) --------------------------------------- */
 /* Raw device pointer + byte size of one all-view buffer, laid out [V][per-view block]:
- * 0 labels i32[H*W], 1 records (SoA block), 2 member offsets i32[nsp+1],
- * 3 member pixels i32[H*W], 4 planes f64x4[nsp], 5 depth f32[H*W].  *view_stride is the
+ * 0 labels i32[H*W], 1 centroid x f64[nsp], 2 centroid y f64[nsp], 3 mean colour f32x4[nsp],
+ * 4 pixel count i32[nsp], 5 member offsets i32[nsp+1], 6 member pixels i32[H*W],
+ * 7 planes f64x4[nsp], 8 depth f32[H*W], 9 centroid rays f64x2[nsp].  *view_stride is the
  * per-view block size in bytes. */
 int lfdg_device_buffer(lfdg_ctx* ctx, int which, void** ptr, size_t* bytes, size_t* view_stride);
 /* After an external all-gather filled buffers of views this context did not compute. */
 int lfdg_mark_views_ready(lfdg_ctx* ctx, int v0, int n, int what);
+
+/* ---- self-test ------------------------------------------------------------------------- */
+/* Device ports of glibc exp / expf used by the energy (glibc_math.cuh), on caller inputs. */
+int lfdg_selftest_exp(int device, const double* in, double* out, size_t n);
+int lfdg_selftest_expf(int device, const float* in, float* out, size_t n);
 
 #ifdef __cplusplus
 }

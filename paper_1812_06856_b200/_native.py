@@ -63,6 +63,7 @@ EXPORTED = [
     "lfdg_set_planes", "lfdg_get_planes", "lfdg_rasterize", "lfdg_rasterize_views", "lfdg_get_depth",
     "lfdg_set_depth", "lfdg_make_refine_context", "lfdg_set_refine_views", "lfdg_refine_iteration",
     "lfdg_run_refinement", "lfdg_get_min_nb_sim", "lfdg_device_buffer", "lfdg_mark_views_ready",
+    "lfdg_selftest_exp", "lfdg_selftest_expf",
 ]
 
 _lib = None
@@ -134,6 +135,8 @@ def lib():
         "lfdg_get_min_nb_sim": (I, [P, I, P]),
         "lfdg_device_buffer": (I, [P, I, C.POINTER(P), C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
         "lfdg_mark_views_ready": (I, [P, I, I, I]),
+        "lfdg_selftest_exp": (I, [I, P, P, C.c_size_t]),
+        "lfdg_selftest_expf": (I, [I, P, P, C.c_size_t]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

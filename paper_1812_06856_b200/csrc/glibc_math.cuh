@@ -1,0 +1,178 @@
+// Bit-exact ports of the glibc 2.39 exp / expf that the reference calls (x86-64, FMA IFUNC
+// variants __exp_fma / __expf_fma), usable on host and device.
+//
+// Why: the refinement energy (refine.hpp:36 depth_consistency, :149 photo weight, :158
+// visibility) calls std::exp(double) and the colour weights (superpixel.hpp:347) call
+// std::exp(float).  CUDA's exp/expf differ from glibc in the last bit on a fraction of inputs,
+// which would perturb energies and flip near-ties.  These ports reproduce glibc's algorithm
+// (ARM optimized-routines exp/expf, table sizes 128 / 32) with the FMA placement that GCC chose
+// for the FMA variants, read off `objdump -d` of libm.so.6; tables are the
+// libm bytes (libm_tables.h).  tests/test_libm_port.py checks them against the host libm
+// (expf exhaustively over every float, exp on 2e8 samples); tests/test_gpu_math.py on device.
+#pragma once
+
+#include <math.h>
+#include <stdint.h>
+
+#include "libm_tables.h"
+
+#if defined(__CUDACC__)
+#define LFDG_HD __host__ __device__ __forceinline__
+#else
+#define LFDG_HD inline
+#endif
+
+namespace lfdg {
+namespace libm {
+
+#if defined(__CUDACC__)
+__device__ const uint64_t kExpTabDev[256] = LFDG_EXP_TAB_INIT;
+__device__ const uint64_t kExpfTabDev[32] = LFDG_EXPF_TAB_INIT;
+#endif
+static const uint64_t kExpTabHost[256] = LFDG_EXP_TAB_INIT;
+static const uint64_t kExpfTabHost[32] = LFDG_EXPF_TAB_INIT;
+
+LFDG_HD uint64_t exp_tab(unsigned i) {
+#if defined(__CUDA_ARCH__)
+    return __ldg(reinterpret_cast<const unsigned long long*>(&kExpTabDev[i]));
+#else
+    return kExpTabHost[i];
+#endif
+}
+LFDG_HD uint64_t expf_tab(unsigned i) {
+#if defined(__CUDA_ARCH__)
+    return __ldg(reinterpret_cast<const unsigned long long*>(&kExpfTabDev[i]));
+#else
+    return kExpfTabHost[i];
+#endif
+}
+
+LFDG_HD uint64_t as_u64(double x) {
+#if defined(__CUDA_ARCH__)
+    return (uint64_t)__double_as_longlong(x);
+#else
+    union {
+        double d;
+        uint64_t u;
+    } v;
+    v.d = x;
+    return v.u;
+#endif
+}
+LFDG_HD double as_f64(uint64_t x) {
+#if defined(__CUDA_ARCH__)
+    return __longlong_as_double((long long)x);
+#else
+    union {
+        double d;
+        uint64_t u;
+    } v;
+    v.u = x;
+    return v.d;
+#endif
+}
+LFDG_HD uint32_t as_u32(float x) {
+#if defined(__CUDA_ARCH__)
+    return (uint32_t)__float_as_uint(x);
+#else
+    union {
+        float f;
+        uint32_t u;
+    } v;
+    v.f = x;
+    return v.u;
+#endif
+}
+
+LFDG_HD double fma_(double a, double b, double c) {
+#if defined(__CUDA_ARCH__)
+    return __fma_rn(a, b, c);
+#else
+    return fma(a, b, c);
+#endif
+}
+
+// __exp_fma (glibc sysdeps/ieee754/dbl-64/e_exp.c, x86-64 FMA build).
+LFDG_HD double exp(double x) {
+    const double kInvLn2N = 0x1.71547652b82fep+7;
+    const double kShift = 0x1.8p+52;
+    const double kNegLn2hiN = -0x1.62e42fefa0000p-8;
+    const double kNegLn2loN = -0x1.cf79abc9e3b3ap-47;
+    const double C2 = 0x1.ffffffffffdbdp-2, C3 = 0x1.555555555543cp-3;
+    const double C4 = 0x1.55555cf172b91p-5, C5 = 0x1.1111167a4d017p-7;
+    const uint64_t ux = as_u64(x);
+    uint32_t abstop = (uint32_t)(ux >> 52) & 0x7ff;
+    if (abstop - 0x3c9u > 0x3eu) {
+        if ((int32_t)(abstop - 0x3c9u) < 0) return 1.0 + x;  // |x| < 2^-54
+        if (abstop > 0x408u) {                                 // |x| >= 1024
+            if (ux == 0xfff0000000000000ull) return 0.0;
+            if (abstop == 0x7ffu) return 1.0 + x;
+            if (ux >> 63) return 0.0;       // __math_uflow: 0x1p-767 * 0x1p-767
+            return as_f64(0x7ff0000000000000ull);  // __math_oflow
+        }
+        abstop = 0;  // 512 <= |x| < 1024: specialcase below
+    }
+    double kd = fma_(x, kInvLn2N, kShift);  // z = InvLn2N * x; kd = z + Shift (contracted)
+    const uint64_t ki = as_u64(kd);
+    kd = kd - kShift;
+    const double r = fma_(kd, kNegLn2loN, fma_(kd, kNegLn2hiN, x));
+    const unsigned idx = 2u * (unsigned)(ki & 127u);
+    const uint64_t top = ki << 45;
+    const double tail = as_f64(exp_tab(idx));
+    uint64_t sbits = exp_tab(idx + 1) + top;
+    const double r2 = r * r;
+    const double tmp = fma_(r2 * r2, fma_(r, C5, C4), fma_(fma_(r, C3, C2), r2, r + tail));
+    if (abstop == 0) {
+        if ((ki & 0x80000000ull) == 0) {
+            sbits -= 1009ull << 52;
+            const double scale = as_f64(sbits);
+            return 0x1p1009 * fma_(scale, tmp, scale);
+        }
+        sbits += 1022ull << 52;
+        const double scale = as_f64(sbits);
+        const double t = scale * tmp;
+        double y = scale + t;
+        if (y < 1.0) {
+            const double hi = y + 1.0;
+            double lo = (scale - y) + t;
+            lo = ((1.0 - hi) + y) + lo;
+            y = (lo + hi) - 1.0;
+            if (y == 0.0) y = 0.0;
+        }
+        return 0x1p-1022 * y;
+    }
+    const double scale = as_f64(sbits);
+    return fma_(scale, tmp, scale);
+}
+
+// __expf_fma (glibc sysdeps/ieee754/flt-32/e_expf.c, x86-64 FMA build).
+LFDG_HD float expf(float x) {
+    const double kShift = 0x1.8p+52;
+    const double kInvLn2N = 0x1.71547652b82fep+5;
+    const double C0 = 0x1.c6af84b912394p-20, C1 = 0x1.ebfce50fac4f3p-13, C2 = 0x1.62e42ff0c52d6p-6;
+    const uint32_t ux = as_u32(x);
+    const uint32_t abstop = (ux >> 20) & 0x7ff;
+    const double xd = (double)x;
+    if (abstop > 0x42au) {
+        if (ux == 0xff800000u) return 0.0f;
+        if (abstop > 0x7f7u) return x + x;
+        if (x > 0x1.62e42ep6f) return (float)as_f64(0x7ff0000000000000ull);  // __math_oflowf
+        if (x < -0x1.9fe368p6f) return 0.0f;                                // __math_uflowf
+        if (x < -0x1.9d1d9ep6f) return 0x1p-149f;  // __math_may_uflowf: 0x1.4p-75f * 0x1.4p-75f
+    }
+    double kd = fma_(kInvLn2N, xd, kShift);
+    const uint64_t ki = as_u64(kd);
+    kd = kd - kShift;
+    const double r = fma_(kInvLn2N, xd, -kd);
+    const uint64_t t = expf_tab((unsigned)(ki & 31u)) + (ki << 47);
+    const double s = as_f64(t);
+    const double z = fma_(r, C0, C1);
+    const double r2 = r * r;
+    double y = fma_(r, C2, 1.0);
+    y = fma_(z, r2, y);
+    y = y * s;
+    return (float)y;
+}
+
+}  // namespace libm
+}  // namespace lfdg

@@ -52,3 +52,27 @@ def test_rasterize_bit_exact(c1):
     dc.rasterize()
     for v in range(3):
         assert np.array_equal(dc.get_depth(v), rs.depth(v))
+
+
+def test_refine_bit_exact(c1):
+    """refine_iteration x3 (+ rasterize) in lockstep: planes, depth rasters and RefineStats."""
+    from paper_1812_06856_b200 import api
+
+    sc, rs, dc = c1
+    # both sides start from the same (bit-identical) init state of the tests above
+    sigma_r, k_r = rs.refine_context(32, iterations=3)
+    sigma_g, k_g = dc.make_refine_context(api.EnergyParams(iterations=3), 32)
+    assert sigma_r == sigma_g and k_r == k_g
+    for v in range(3):
+        assert np.array_equal(dc.min_nb_sim(v), rs.min_nb_sim(v, len(dc.get_planes(v))))
+    for l in range(1, 4):
+        acc_r, vio_r = rs.refine_iteration(l, with_stats=True)
+        acc_g, vio_g = dc.refine_iteration(l)
+        rs.rasterize()
+        dc.rasterize()
+        for v in range(3):
+            want, got = rs.planes(v), dc.get_planes(v)
+            bad = np.any(got != want, axis=1)
+            assert not bad.any(), f"iteration {l} view {v}: {bad.sum()} planes differ, first {np.argmax(bad)}"
+            assert np.array_equal(dc.get_depth(v), rs.depth(v))
+        assert (acc_g, vio_g) == (acc_r, vio_r)
