@@ -167,6 +167,18 @@ int lfdg_device_buffer(lfdg_ctx* ctx, int which, void** ptr, size_t* bytes, size
 /* After an external all-gather filled buffers of views this context did not compute. */
 int lfdg_mark_views_ready(lfdg_ctx* ctx, int v0, int n, int what);
 
+/* ---- synthetic scenes (fixtures.hpp restated; host code, no GPU needed) ------------------ */
+/* kind: 0 cluttered_scene, 1 staircase_scene, 2 wall_scene(depth = extra), 3 slanted_scene
+ * (tilt_deg = extra), 4 occluder_scene; grid_nx > 0 replaces the rig by make_grid_rig(grid_nx,
+ * grid_ny, f, baseline, W, H).  V = grid_nx * grid_ny or n_views.  Outputs (NULL allowed):
+ * scaled-LAB and RGB [V][H][W][3], ground-truth depth [V][H][W], cameras [V], range[2].
+ * threads <= 0: all hardware threads (the result does not depend on it). */
+int lfdg_render_scene(int kind, int n_views, int width, int height, double f, double baseline, double extra,
+                      int grid_nx, int grid_ny, int threads, float* lab_out, float* rgb_out, float* gt_out,
+                      lfdg_camera* cams_out, double* range_out);
+/* rgb_to_scaled_lab (image.hpp:83-107) over n pixels of [n][3] floats. */
+int lfdg_rgb_to_scaled_lab(int64_t n_pixels, const float* rgb, float* lab);
+
 /* ---- self-test ------------------------------------------------------------------------- */
 /* Device ports of glibc exp / expf used by the energy (glibc_math.cuh), on caller inputs. */
 int lfdg_selftest_exp(int device, const double* in, double* out, size_t n);

@@ -63,7 +63,7 @@ EXPORTED = [
     "lfdg_set_planes", "lfdg_get_planes", "lfdg_rasterize", "lfdg_rasterize_views", "lfdg_get_depth",
     "lfdg_set_depth", "lfdg_make_refine_context", "lfdg_set_refine_views", "lfdg_refine_iteration",
     "lfdg_run_refinement", "lfdg_get_min_nb_sim", "lfdg_device_buffer", "lfdg_mark_views_ready",
-    "lfdg_selftest_exp", "lfdg_selftest_expf",
+    "lfdg_selftest_exp", "lfdg_selftest_expf", "lfdg_render_scene", "lfdg_rgb_to_scaled_lab",
 ]
 
 _lib = None
@@ -137,6 +137,8 @@ def lib():
         "lfdg_mark_views_ready": (I, [P, I, I, I]),
         "lfdg_selftest_exp": (I, [I, P, P, C.c_size_t]),
         "lfdg_selftest_expf": (I, [I, P, P, C.c_size_t]),
+        "lfdg_render_scene": (I, [I, I, I, I, D, D, D, I, I, I, P, P, P, P, P]),
+        "lfdg_rgb_to_scaled_lab": (I, [C.c_int64, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
