@@ -140,6 +140,14 @@ int lfdg_rasterize_views(lfdg_ctx* ctx, int v0, int n);
 int lfdg_get_depth(lfdg_ctx* ctx, int view, float* depth);
 int lfdg_set_depth(lfdg_ctx* ctx, int view, const float* depth);
 
+/* ---- end-to-end transfers ----------------------------------------------------------------- */
+/* Enqueue the upload of views [v0, v0+n) from host [n][H][W][3] scaled-LAB floats (pinned memory
+ * makes it one async DMA); the images replace the context's copies. */
+int lfdg_upload_images(lfdg_ctx* ctx, int v0, int n, const float* images);
+/* Enqueue the download of planes [n][nsp] and depth [n][H][W] of views [v0, v0+n) (either may be
+ * NULL); sync != 0 waits for completion. */
+int lfdg_download_results(lfdg_ctx* ctx, int v0, int n, lfdg_plane* planes, float* depth, int sync);
+
 /* ---- refinement (refine.hpp:53, :253, :325) ----------------------------------------------- */
 /* make_refine_context: resolves sigma (0 → 1.5·inverse_depth_step) and size_init (0 → min(W,H))
  * exactly as refine.hpp:56-57 and builds the static tables on the device. */
@@ -154,6 +162,9 @@ int lfdg_set_refine_views(lfdg_ctx* ctx, int v0, int n);
 int lfdg_refine_iteration(lfdg_ctx* ctx, int l, uint64_t* accepted, uint64_t* violations);
 /* run_refinement: l = 1..iterations of (refine_iteration; rasterize). */
 int lfdg_run_refinement(lfdg_ctx* ctx, uint64_t* accepted, uint64_t* violations);
+/* Work counters accumulated by refine_iteration since the last reset: evaluated
+ * (candidate, target, member pixel) triples of pair_stats and evaluated candidates. */
+int lfdg_refine_work(lfdg_ctx* ctx, uint64_t* pixel_evals, uint64_t* candidate_evals, int reset);
 /* min_neighbor_similarity table of make_refine_context (refine.hpp:71), [nsp] floats. */
 int lfdg_get_min_nb_sim(lfdg_ctx* ctx, int view, float* out);
 
@@ -183,6 +194,8 @@ int lfdg_rgb_to_scaled_lab(int64_t n_pixels, const float* rgb, float* lab);
 /* Device ports of glibc exp / expf used by the energy (glibc_math.cuh), on caller inputs. */
 int lfdg_selftest_exp(int device, const double* in, double* out, size_t n);
 int lfdg_selftest_expf(int device, const float* in, float* out, size_t n);
+/* Measured FP64 FMA throughput of the device (FLOP/s, DFMA = 2), the sweep/refine roofline. */
+int lfdg_selftest_fp64_peak(int device, double* flops);
 
 #ifdef __cplusplus
 }

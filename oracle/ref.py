@@ -78,6 +78,8 @@ def lib():
     L.ref_pair_stats.argtypes = [P, I, I, P, I, P]
     L.ref_normal_candidates.argtypes = [P, I, I, P]
     L.ref_grid_neighbors.argtypes = [P, I, I, I, I, I, P]
+    L.ref_sweep_sample.argtypes = [P, I, P, I, I, F, I, U64, I, P]
+    L.ref_refine_tasks.argtypes = [P, I, P, P, I, I, P, P, P, P]
     L.ref_bad_pixel_rate.restype = D
     L.ref_bad_pixel_rate.argtypes = [I, I, I, P, P, I, P, D, D, D, I, D]
     _lib = L
@@ -141,6 +143,25 @@ class Session:
         mem = np.zeros(self.H * self.W, np.int32)
         self.L.ref_get_grid(self.h, view, _p(labels), _p(rec), _p(off), _p(mem))
         return dict(labels=labels, records=rec, offsets=off, members=mem, grid_w=gw.value, grid_h=gh.value)
+
+    def sweep_sample(self, view, sps, levels, threshold=0.05, max_neighbors=0, seed=0, workers=1):
+        sps = np.ascontiguousarray(sps, np.int32)
+        out = np.zeros((len(sps), 4), np.float64)
+        _check(self.L.ref_sweep_sample(self.h, view, _p(sps), len(sps), levels, threshold, max_neighbors, seed,
+                                       workers, _p(out)))
+        return out
+
+    def refine_tasks(self, l, views, sps, workers=1, counts=False):
+        """refine_iteration's task body on the listed tasks -> (planes, accepted[, cons_evals, pixel_evals])."""
+        views = np.ascontiguousarray(views, np.int32)
+        sps = np.ascontiguousarray(sps, np.int32)
+        out = np.zeros((len(sps), 4), np.float64)
+        acc = np.zeros(3, np.uint64)
+        _check(self.L.ref_refine_tasks(self.h, l, _p(views), _p(sps), len(sps), workers, _p(out), _p(acc[0:1]),
+                                       _p(acc[1:2]), _p(acc[2:3])))
+        if counts:
+            return out, int(acc[0]), int(acc[1]), int(acc[2])
+        return out, int(acc[0])
 
     def matching_views(self, view, max_neighbors=0):
         out = np.zeros(self.V, np.int32)

@@ -10,6 +10,7 @@
 // inc/refine.hpp make_refine_context/refine_iteration/energy, inc/fixtures.hpp scenes,
 // inc/image.hpp rgb_to_scaled_lab, inc/eval.hpp bad_pixel_rate/compute_nocc_mask).
 #include <cstdint>
+#include <atomic>
 #include <cstring>
 #include <memory>
 #include <optional>
@@ -387,6 +388,108 @@ double ref_bad_pixel_rate(int n_views, int width, int height, const float* gt_al
     } catch (const EmptyRegion&) {
         return -1.0;
     }
+}
+
+
+// ---- bounded samples of the reference's per-task loop bodies (bench.py reference arm) -----
+//
+// sweep_view's task body (sweep.hpp:119-137) for a list of superpixels, parallel over
+// `workers` with the reference's own parallel_for; planes_out receives the winners.
+int ref_sweep_sample(void* p, int view, const int* sps, int n, int levels, float threshold, int max_neighbors,
+                     std::uint64_t seed, int workers, double* planes_out) {
+    auto* s = static_cast<Session*>(p);
+    return guarded([&] {
+        SweepParams prm;
+        prm.levels = levels;
+        prm.tssd_threshold = threshold;
+        prm.max_neighbors = max_neighbors;
+        prm.validate();
+        const std::vector<int> targets = matching_views(s->mvs, view, prm.max_neighbors);
+        parallel_for(static_cast<std::size_t>(n), workers, [&](std::size_t task) {
+            const std::int32_t sp = sps[task];
+            RandomStream rng = derive_stream(seed, static_cast<std::uint64_t>(view), static_cast<std::uint64_t>(sp));
+            const std::vector<double> depths = sample_inverse_depths(s->mvs.range, prm.levels, rng);
+            double best_cost = 0, best_depth = 0;
+            bool first = true;
+            for (auto it = depths.rbegin(); it != depths.rend(); ++it) {
+                const double c = sweep_cost(s->mvs, s->grids, view, sp, *it, targets, prm.tssd_threshold);
+                if (first || c < best_cost || (c == best_cost && *it < best_depth)) {
+                    best_cost = c;
+                    best_depth = *it;
+                    first = false;
+                }
+            }
+            plane_to(SuperpixelPlane{best_depth, Vec3(0, 0, -1)}, planes_out + 4 * task);
+        });
+    });
+}
+
+// refine_iteration's task body (refine.hpp:269-320) for a list of (view, sp) tasks, built from
+// the reference's public term functions exactly as the lambda composes them; parallel over
+// `workers`.  Writes the new planes and the accepted count (no violation re-check, like the
+// pipeline's stats-free call at pipeline.hpp:370).
+int ref_refine_tasks(void* p, int l, const int* views, const int* sps, int n, int workers, double* planes_out,
+                     std::uint64_t* accepted, std::uint64_t* consistency_evals, std::uint64_t* pixel_evals) {
+    auto* s = static_cast<Session*>(p);
+    return guarded([&] {
+        const RefineContext& ctx = *s->ctx;
+        const MultiViewSet& mvs = *ctx.mvs;
+        const PlaneMap& state = s->state;
+        const int kernel_px = static_cast<int>(ctx.params.size_init / static_cast<double>(l));
+        const int kernel_step =
+            std::max(1, static_cast<int>(std::lround(ctx.params.steps_init / static_cast<double>(l))));
+        const double max_consistency = ctx.params.use_occlusion ? 1.0 + ctx.params.eta : 1.0;
+        std::atomic<std::uint64_t> acc{0}, cev{0}, pev{0};
+        parallel_for(static_cast<std::size_t>(n), workers, [&](std::size_t task) {
+            const int v = views[task];
+            const std::int32_t sp = sps[task];
+            const SuperpixelGrid& grid = ctx.grid(v);
+            const PinholeCamera& cam = mvs.cameras[v];
+            const Vec2 centroid(grid.sp[sp].cx, grid.sp[sp].cy);
+            SuperpixelPlane current = state.planes[v][sp];
+            const std::uint64_t task_pix = grid.pixels[sp].size() * ctx.targets[v].size();
+            double e_cur = energy(ctx, v, sp, current, state);
+            if (ctx.params.use_consistency) {
+                cev.fetch_add(1, std::memory_order_relaxed);
+                pev.fetch_add(task_pix, std::memory_order_relaxed);
+            }
+            auto accept_if_better = [&](const SuperpixelPlane& cand, double e) {
+                if (!(e > e_cur)) return;
+                acc.fetch_add(1, std::memory_order_relaxed);
+                current = cand;
+                e_cur = e;
+            };
+            auto try_candidate = [&](const SuperpixelPlane& cand) {
+                if (cand.depth == current.depth && cand.normal == current.normal) return;
+                if (cand.depth < mvs.range.d_min || cand.depth > mvs.range.d_max) return;
+                if (ctx.params.use_smoothness && ctx.params.use_consistency) {
+                    const double es = smoothness_term(ctx, v, sp, cand, state);
+                    if (es * max_consistency <= e_cur) return;
+                    cev.fetch_add(1, std::memory_order_relaxed);
+                    pev.fetch_add(task_pix, std::memory_order_relaxed);
+                    accept_if_better(cand, es * consistency_term(ctx, v, sp, cand, state));
+                    return;
+                }
+                if (ctx.params.use_consistency) {
+                    cev.fetch_add(1, std::memory_order_relaxed);
+                    pev.fetch_add(task_pix, std::memory_order_relaxed);
+                }
+                accept_if_better(cand, energy(ctx, v, sp, cand, state));
+            };
+            for (const std::int32_t nb : grid_neighbors(grid, sp, NeighborPattern::Kernel, kernel_px, kernel_step)) {
+                const SuperpixelPlane& nb_plane = state.planes[v][nb];
+                const Vec2 nb_centroid(grid.sp[nb].cx, grid.sp[nb].cy);
+                const auto d = plane_depth_at(cam, nb_plane, nb_centroid, centroid);
+                if (!d || *d <= 0) continue;
+                try_candidate(SuperpixelPlane{*d, nb_plane.normal});
+            }
+            for (const Vec3& nrm : normal_candidates(ctx, v, sp, state)) try_candidate(SuperpixelPlane{current.depth, nrm});
+            plane_to(current, planes_out + 4 * task);
+        });
+        if (accepted) *accepted = acc.load();
+        if (consistency_evals) *consistency_evals = cev.load();
+        if (pixel_evals) *pixel_evals = pev.load();
+    });
 }
 
 }  // extern "C"

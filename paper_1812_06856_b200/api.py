@@ -290,6 +290,12 @@ class DeviceContext:
         N.check(self.L.lfdg_run_refinement(self.h, C.byref(a), C.byref(v)))
         return a.value, v.value
 
+    def refine_work(self, reset: bool = True):
+        """(pixel-evals, candidate evals) of pair_stats since the last reset."""
+        a, b = C.c_uint64(), C.c_uint64()
+        N.check(self.L.lfdg_refine_work(self.h, C.byref(a), C.byref(b), int(reset)))
+        return a.value, b.value
+
     def min_nb_sim(self, view: int) -> np.ndarray:
         gw, gh, _ = self.grid_shape(view)
         out = np.zeros(gw * gh, np.float32)

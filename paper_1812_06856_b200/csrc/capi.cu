@@ -6,9 +6,13 @@
 
 #include "context.h"
 
-namespace {
-
+namespace lfdg {
 thread_local std::string g_last_error;
+void set_last_error(const char* m) { g_last_error = m; }
+}  // namespace lfdg
+
+namespace {
+using lfdg::g_last_error;
 
 template <typename Fn>
 int guarded(Fn&& fn) {
@@ -62,7 +66,7 @@ int lfdg_create(int device, lfdg_ctx** out) {
         }
         c->stream = c->own_stream;
         cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
-        c->counters.alloc(2);
+        c->counters.alloc(4);
         *out = reinterpret_cast<lfdg_ctx*>(c);
     });
 }
@@ -130,15 +134,8 @@ int lfdg_set_views(lfdg_ctx* p, int n_views, int width, int height, const float*
         c->refine_n = -1;
         c->depth.alloc((size_t)n_views * hw);
         LFDG_CUDA_CHECK(cudaMemsetAsync(c->depth.p, 0, (size_t)n_views * hw * sizeof(float), c->stream));
-        // Host [V][H][W][3] float -> device float4 (pad w = 0), staged through pinned memory.
-        std::vector<float4> tmp(hw);
-        for (int v = 0; v < n_views; ++v) {
-            const float* src = images + (size_t)v * hw * 3;
-            for (size_t i = 0; i < hw; ++i) tmp[i] = make_float4(src[3 * i], src[3 * i + 1], src[3 * i + 2], 0.f);
-            LFDG_CUDA_CHECK(cudaMemcpyAsync(c->lab.p + (size_t)v * hw, tmp.data(), hw * sizeof(float4),
-                                            cudaMemcpyHostToDevice, c->stream));
-            LFDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
-        }
+        lfdg::upload_images(*c, 0, n_views, images);
+        LFDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
     });
 }
 
@@ -148,15 +145,8 @@ int lfdg_update_images(lfdg_ctx* p, int v0, int n, const float* images) {
         activate(c);
         c->require_views();
         if (v0 < 0 || n < 0 || v0 + n > c->V) throw lfdg::Error(LFDG_STATE, "view range out of bounds");
-        const size_t hw = c->hw();
-        std::vector<float4> tmp(hw);
-        for (int b = 0; b < n; ++b) {
-            const float* src = images + (size_t)b * hw * 3;
-            for (size_t i = 0; i < hw; ++i) tmp[i] = make_float4(src[3 * i], src[3 * i + 1], src[3 * i + 2], 0.f);
-            LFDG_CUDA_CHECK(cudaMemcpyAsync(c->lab.p + (size_t)(v0 + b) * hw, tmp.data(), hw * sizeof(float4),
-                                            cudaMemcpyHostToDevice, c->stream));
-            LFDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
-        }
+        lfdg::upload_images(*c, v0, n, images);
+        LFDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
     });
 }
 
@@ -363,7 +353,7 @@ int lfdg_refine_iteration(lfdg_ctx* p, int l, uint64_t* accepted, uint64_t* viol
         activate(c);
         if (!c->refine.ready) throw lfdg::Error(LFDG_STATE, "no refine context: call lfdg_make_refine_context");
         if (l < 1) throw lfdg::Error(LFDG_INVALID_PARAMS, "iteration index must be >= 1");
-        LFDG_CUDA_CHECK(cudaMemsetAsync(c->counters.p, 0, 2 * sizeof(unsigned long long), c->stream));
+        LFDG_CUDA_CHECK(cudaMemsetAsync(c->counters.p, 0, 2 * sizeof(unsigned long long), c->stream));  // work counters [2..3] accumulate
         lfdg::refine_iteration(*c, l);
         if (accepted || violations) {
             unsigned long long h[2];
@@ -380,7 +370,7 @@ int lfdg_run_refinement(lfdg_ctx* p, uint64_t* accepted, uint64_t* violations) {
         auto* c = C(p);
         activate(c);
         if (!c->refine.ready) throw lfdg::Error(LFDG_STATE, "no refine context: call lfdg_make_refine_context");
-        LFDG_CUDA_CHECK(cudaMemsetAsync(c->counters.p, 0, 2 * sizeof(unsigned long long), c->stream));
+        LFDG_CUDA_CHECK(cudaMemsetAsync(c->counters.p, 0, 2 * sizeof(unsigned long long), c->stream));  // work counters [2..3] accumulate
         for (int l = 1; l <= c->refine.params.iterations; ++l) {
             lfdg::refine_iteration(*c, l);
             lfdg::rasterize_views(*c, 0, c->V);
@@ -390,6 +380,19 @@ int lfdg_run_refinement(lfdg_ctx* p, uint64_t* accepted, uint64_t* violations) {
         LFDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
         if (accepted) *accepted = h[0];
         if (violations) *violations = h[1];
+    });
+}
+
+int lfdg_refine_work(lfdg_ctx* p, uint64_t* pixel_evals, uint64_t* candidate_evals, int reset) {
+    return guarded([&] {
+        auto* c = C(p);
+        activate(c);
+        unsigned long long h[4];
+        LFDG_CUDA_CHECK(cudaMemcpyAsync(h, c->counters.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+        LFDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        if (pixel_evals) *pixel_evals = h[2];
+        if (candidate_evals) *candidate_evals = h[3];
+        if (reset) LFDG_CUDA_CHECK(cudaMemsetAsync(c->counters.p + 2, 0, 2 * sizeof(unsigned long long), c->stream));
     });
 }
 

@@ -105,7 +105,7 @@ struct Ctx {
     // refinement
     RefineTables refine;
     int refine_v0 = 0, refine_n = -1;  // -1: all views
-    DevBuf<unsigned long long> counters;  // [2]: accepted, violations
+    DevBuf<unsigned long long> counters;  // [4]: accepted, violations, pixel-evals, candidate evals
 
     size_t hw() const { return static_cast<size_t>(W) * H; }
     void require_views() const {
@@ -121,6 +121,8 @@ struct Ctx {
     }
 };
 
+void set_last_error(const char* m);  // capi.cu
+
 // ---- stage entry points (implemented in the .cu files) ----------------------------------
 void ensure_grid_buffers(Ctx& c, int S);
 void slic_views(Ctx& c, int v0, int n, const lfdg_slic_params& p);          // slic.cu
@@ -130,5 +132,7 @@ void rasterize_views(Ctx& c, int v0, int n);                                   /
 std::vector<int> matching_views(const Ctx& c, int view, int max_neighbors);    // sweep.cu
 void make_refine_tables(Ctx& c, const lfdg_energy_params& p, int sweep_levels);  // refine.cu
 void refine_iteration(Ctx& c, int l);                                            // refine.cu
+void upload_images(Ctx& c, int v0, int n, const float* host);                     // transfer.cu
+void download_results(Ctx& c, int v0, int n, lfdg_plane* planes, float* depth);   // transfer.cu
 
 }  // namespace lfdg

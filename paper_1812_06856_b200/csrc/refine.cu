@@ -27,8 +27,6 @@
 namespace lfdg {
 namespace {
 
-constexpr int kThreads = 128;
-constexpr int kMaxCand = 512;  // propagation slots + 8 normals per task (checked on the host)
 
 struct RefineArgs {
     // geometry / images
@@ -78,312 +76,394 @@ __device__ __forceinline__ double depth_consistency(double d1, double d2, double
     return libm::exp(-(r * r) / two_sigma2);
 }
 
-// smoothness_term (refine.hpp:84-100) for candidate plane p of task (v, sp).
-__device__ double smoothness(const RefineArgs& a, int v, int sp, double4 p) {
+// ---- smoothness_term (refine.hpp:84-100), warp-parallel: lanes = (candidate, ring slot k)
+// groups of 8.  Each lane evaluates one ring neighbour; every lane of a group then folds the
+// group's 8 slots in ring order with width-8 shuffles, so wsum / acc are the reference's
+// sequential sums.  Returns the smoothness of the lane's group candidate.
+__device__ __forceinline__ double smoothness_group(const RefineArgs& a, int v, int sp, double4 p, bool active) {
+    const int k = threadIdx.x & 7;
     const int gx = sp % a.gw, gy = sp / a.gw;
-    const double2 cr = a.cray[(size_t)v * a.nsp + sp];
-    const double ax = p.x * cr.x, ay = p.x * cr.y, az = p.x;
-    const double num = (p.y * ax + p.z * ay) + p.w * az;
-    const float* rw = a.ring_w + ((size_t)v * a.nsp + sp) * 8;
-    double wsum = 0, acc = 0;
-    for (int k = 0; k < 8; ++k) {
+    bool present = false, has_c = false;
+    double w = 0, c = 0;
+    if (active) {
         const int nx = gx + kDir[k][0], ny = gy + kDir[k][1];
-        if (nx < 0 || ny < 0 || nx >= a.gw || ny >= a.gh) continue;
-        const int nb = ny * a.gw + nx;
-        const double w = (double)rw[k];
-        wsum += w;
-        const double2 nr = a.cray[(size_t)v * a.nsp + nb];
-        const double denom = (p.y * nr.x + p.z * nr.y) + p.w;
-        if (fabs(denom) <= 1e-9) continue;
-        const double ext = num / denom;
-        if (ext <= 0) continue;
-        acc += w * depth_consistency(a.planes[(size_t)v * a.nsp + nb].x, ext, a.two_sigma2);
+        if (nx >= 0 && ny >= 0 && nx < a.gw && ny < a.gh) {
+            present = true;
+            const int nb = ny * a.gw + nx;
+            w = (double)a.ring_w[((size_t)v * a.nsp + sp) * 8 + k];
+            const double2 cr = a.cray[(size_t)v * a.nsp + sp];
+            const double ax = p.x * cr.x, ay = p.x * cr.y, az = p.x;
+            const double num = (p.y * ax + p.z * ay) + p.w * az;
+            const double2 nr = a.cray[(size_t)v * a.nsp + nb];
+            const double denom = (p.y * nr.x + p.z * nr.y) + p.w;
+            if (!(fabs(denom) <= 1e-9)) {
+                const double ext = num / denom;
+                if (ext > 0) {
+                    has_c = true;
+                    c = w * depth_consistency(a.planes[(size_t)v * a.nsp + nb].x, ext, a.two_sigma2);
+                }
+            }
+        }
+    }
+    double wsum = 0, acc = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const double wj = __shfl_sync(LFDG_FULL_MASK, w, j, 8);
+        const double cj = __shfl_sync(LFDG_FULL_MASK, c, j, 8);
+        const int pj = __shfl_sync(LFDG_FULL_MASK, (int)present, j, 8);
+        const int hj = __shfl_sync(LFDG_FULL_MASK, (int)has_c, j, 8);
+        if (pj) wsum += wj;
+        if (hj) acc += cj;
     }
     if (wsum <= 1e-30) return 1.0;
     return acc / wsum;
 }
 
-// pair_stats (refine.hpp:111-172) -> visibility + occlusion, for one (candidate, target).
-__device__ double pair_contrib(const RefineArgs& a, int v, int sp, double4 p, int ti) {
-    const int t = a.targets[(size_t)v * a.N + ti];
-    const double* rel = a.rel + ((size_t)v * a.N + ti) * 12;
-    const double R0 = rel[0], R1 = rel[1], R2 = rel[2], R3 = rel[3], R4 = rel[4], R5 = rel[5];
-    const double R6 = rel[6], R7 = rel[7], R8 = rel[8], T0 = rel[9], T1 = rel[10], T2 = rel[11];
-    const Cam& tc = a.cams[t];
-    const double K00 = tc.K[0], K01 = tc.K[1], K02 = tc.K[2], K11 = tc.K[4], K12 = tc.K[5];
+// lround(q) for q = hx / z computed as hx * (1/z): exact whenever q is farther than 8x the
+// product's error bound (2^-52 |q|) from a rounding boundary (a half-integer); otherwise the
+// caller falls back to the true division.  Returns false when the fast value cannot be used.
+__device__ __forceinline__ bool fast_lround(double q, int& out) {
+    const double aq = fabs(q);
+    if (!(aq < 0x1p30)) return false;
+    const double f = q - floor(q);
+    if (fabs(f - 0.5) <= aq * 0x1p-49 + 0x1p-1000) return false;
+    out = (int)llround(q);
+    return true;
+}
+
+// Per-warp shared-memory slice.  Candidate planes / upper bounds live in a per-warp global
+// scratch row (L1-resident); the pixel-term tiles are shared memory.
+struct WarpSmem {
+    double4* cand;  // [cap]   (global scratch)
+    double* es;     // [cap]   (global scratch)
+    double* ph;     // [32][pitch] photo term of (pixel j, target tt): weight, or -1 (no sample)
+    double* vs;     // [32][pitch] visibility term: Gaussian (visible), -1 (occluded), -2 (no target depth)
+    double* res;    // [kResCap] V + O per target
+    int pitch;
+};
+constexpr int kResCap = 128;
+
+__host__ __device__ inline int tile_pitch(int N) {
+    const int nr = N < 32 ? N : 32;
+    return (nr & 1) ? nr : nr + 1;  // odd pitch: conflict-free column reads, 2-way row writes
+}
+__host__ __device__ inline size_t warp_smem_bytes(int N) {
+    const size_t b = 2 * 32 * (size_t)tile_pitch(N) * sizeof(double) + kResCap * sizeof(double);
+    return (b + 127) & ~(size_t)127;
+}
+
+// consistency_term (refine.hpp:189-199) of plane p for task (v, sp), one warp.
+// Lanes own 32 consecutive member pixels at a time (coherent branches, coalesced ray loads,
+// neighbouring gathers) and loop over the targets; the per-(pixel, target) terms go to a
+// shared tile, then lane t folds target t's column in member order — the reference's
+// sequential photo_sum / vis_sum / x_count / y_nonempty of pair_stats (refine.hpp:127-163),
+// bit for bit.  Finally V + O are summed in target order (refine.hpp:193-198).
+template <bool kIdR, bool kCanonK>
+__device__ __forceinline__ double consistency_warp(const RefineArgs& a, const WarpSmem& w, int v, int sp, double4 p, int m0, int n) {
+    const int lane = threadIdx.x & 31;
+    const int N = a.N;
+    if (N == 0) return 1.0;
     const size_t hw = (size_t)a.W * a.H;
-    const int32_t* tl = a.labels + (size_t)t * hw;
-    const float* tdep = a.depth + (size_t)t * hw;
-    const float4* tcol = a.color + (size_t)t * a.nsp;
     const float4 rc = a.color[(size_t)v * a.nsp + sp];
     const double2 cr = a.cray[(size_t)v * a.nsp + sp];
     const double ax = p.x * cr.x, ay = p.x * cr.y, az = p.x;
     const double plane_num = (p.y * ax + p.z * ay) + p.w * az;
-    const int m0 = a.moff[(size_t)v * (a.nsp + 1) + sp];
-    const int n = a.moff[(size_t)v * (a.nsp + 1) + sp + 1] - m0;
     const double2* mr = a.mray + (size_t)v * hw + m0;
-
-    double photo_sum = 0, vis_sum = 0;
-    int x_count = 0;
-    bool y_nonempty = false;
-    int cached_label = -1;
-    double cached_w = 0;
-    for (int i = 0; i < n; ++i) {
-        const double2 r = mr[i];
-        const double denom = (p.y * r.x + p.z * r.y) + p.w;
-        if (fabs(denom) <= 1e-9) continue;
-        const double s = plane_num / denom;
-        if (s <= 0) continue;
-        const double sv0 = s * r.x, sv1 = s * r.y, sv2 = s;
-        const double x0 = ((R0 * sv0 + R1 * sv1) + R2 * sv2) + T0;
-        const double x1 = ((R3 * sv0 + R4 * sv1) + R5 * sv2) + T1;
-        const double x2 = ((R6 * sv0 + R7 * sv1) + R8 * sv2) + T2;
-        if (x2 <= 0) continue;
-        const double u = ((K00 * x0 + K01 * x1) + K02 * x2) / x2;
-        const double w = (K11 * x1 + K12 * x2) / x2;
-        const int px = lround_int(u);
-        const int py = lround_int(w);
-        if (px < 0 || py < 0 || px >= a.W || py >= a.H) continue;
-        const size_t q = (size_t)py * a.W + px;
-        const int tlab = tl[q];
-        if (tlab != cached_label) {
-            cached_label = tlab;
-            const float4 c = tcol[tlab];
-            cached_w = libm::exp(-(double)color_dist2(rc.x, rc.y, rc.z, c.x, c.y, c.z) * a.inv_two_alpha2);
-        }
-        photo_sum += cached_w;
-        const float td = tdep[q];
-        if (td <= 0) continue;
-        if (x2 <= (double)td * (1.0 + 1e-6)) {
-            const double rr = 1.0 / x2 - 1.0 / (double)td;
-            vis_sum += libm::exp(-rr * rr * a.inv_two_sigma2);
-            ++x_count;
-        } else {
-            y_nonempty = true;
-        }
-    }
-    const double photo = photo_sum / (double)n;
-    const double vis = x_count > 0 ? photo * (vis_sum / x_count) : 0.0;
-    double occ = 0.0;
-    if (a.use_o && y_nonempty) occ = a.eta * (1.0 - (double)a.min_nb_sim[(size_t)v * a.nsp + sp]);
-    return vis + occ;
-}
-
-struct Shared {
-    double4 cand[kMaxCand];
-    double es[kMaxCand];
-    int sel[kThreads];
-    double res[kThreads];  // per (chunk candidate, target) contribution
-    double e_chunk[kThreads];
-    int scan[kThreads];
-    double4 current;
-    double e_cur;
-    int n_cand;
-    int nsel;
-    int next;
-    unsigned accepted;
-};
-
-// Evaluate candidates [0, n_cand) of s.cand in chunks (see file comment).  Thread 0 owns
-// s.current / s.e_cur.  `first_is_current`: s.cand[0] is the current plane and its energy
-// initialises e_cur (refine.hpp:277) without an acceptance test.
-__device__ void run_candidates(const RefineArgs& a, Shared& s, int v, int sp, bool init_pass) {
-    const int tid = threadIdx.x;
-    const int N = a.N;
-    const int K = N > 0 ? max(1, kThreads / N) : kThreads;
-    const bool prune = a.use_s && a.use_c;
-    if (tid == 0) s.next = 0;
-    __syncthreads();
-    while (true) {
-        if (tid == 0) {
-            int k = 0, nx = s.next;
-            while (nx < s.n_cand && k < K) {
-                if (init_pass || !prune || s.es[nx] * a.max_consistency > s.e_cur) s.sel[k++] = nx;
-                ++nx;
-            }
-            s.next = nx;
-            s.nsel = k;
-        }
-        __syncthreads();
-        const int nsel = s.nsel;
-        if (nsel == 0) break;
-        if (a.use_c && N > 0) {
-            if (tid < nsel * N) {
-                const int ci = tid / N, ti = tid % N;
-                s.res[tid] = pair_contrib(a, v, sp, s.cand[s.sel[ci]], ti);
-            }
-            __syncthreads();
-        }
-        if (tid < nsel) {
-            const int c = s.sel[tid];
-            double e;
-            if (a.use_c) {
-                double ec = 1.0;
-                if (N > 0) {
-                    double acc = 0;
-                    for (int ti = 0; ti < N; ++ti) acc += s.res[tid * N + ti];
-                    ec = acc / (double)N;
-                }
-                e = prune ? s.es[c] * ec : (a.use_s ? 1.0 * s.es[c] : 1.0) * ec;
-            } else {
-                e = a.use_s ? 1.0 * s.es[c] : 1.0;
-            }
-            s.e_chunk[tid] = e;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            for (int ci = 0; ci < nsel; ++ci) {
-                const double e = s.e_chunk[ci];
-                if (init_pass) {
-                    s.e_cur = e;
-                } else if (e > s.e_cur) {
-                    s.e_cur = e;
-                    s.current = s.cand[s.sel[ci]];
-                    s.accepted++;
-                }
-            }
-        }
-        __syncthreads();
-    }
-}
-
-__global__ void __launch_bounds__(kThreads) k_refine(RefineArgs a) {
-    __shared__ Shared s;
-    const int tid = threadIdx.x;
-    const int task = blockIdx.x;
-    const int v = a.rv0 + task / a.nsp;
-    const int sp = task % a.nsp;
-    const size_t vs = (size_t)v * a.nsp;
-    const double4 cur0 = a.planes[vs + sp];
-    if (tid == 0) {
-        s.current = cur0;
-        s.accepted = 0;
-        s.n_cand = 1;
-        s.cand[0] = cur0;
-    }
-    __syncthreads();
-    // ---- e_cur = energy(current) (refine.hpp:277)
-    if (tid == 0 && a.use_s) s.es[0] = smoothness(a, v, sp, cur0);
-    __syncthreads();
-    run_candidates(a, s, v, sp, true);
-
-    // ---- phase A: propagation candidates in grid_neighbors(Kernel) order (superpixel.hpp:318-343)
-    const int gx = sp % a.gw, gy = sp / a.gw;
-    const double2 crs = a.cray[vs + sp];
-    int base = 0;
-    for (int s0 = 0; s0 < a.n_slots; s0 += kThreads) {
-        const int slot = s0 + tid;
-        bool ok = false;
-        double4 cand = make_double4(0, 0, 0, 0);
-        if (slot < a.n_slots) {
-            int dx, dy;
-            if (slot < 8) {
-                dx = kDir[slot][0];
-                dy = kDir[slot][1];
-            } else {
-                const int k = (slot - 8) / a.per_dir;   // direction (kDir order)
-                const int ri = (slot - 8) % a.per_dir;  // radius-minor: r = step, 2 step, ... <= radius_sp
-                const int r = a.kernel_step * (ri + 1);
-                dx = kDir[k][0] * r;
-                dy = kDir[k][1] * r;
-                if (abs(dx) <= 1 && abs(dy) <= 1) dx = 1 << 20;  // already in the ring (superpixel.hpp:334)
-            }
-            const int nx = gx + dx, ny = gy + dy;
-            if (nx >= 0 && ny >= 0 && nx < a.gw && ny < a.gh) {
-                const int nb = ny * a.gw + nx;
-                const double4 np = a.planes[vs + nb];
-                const double2 nr = a.cray[vs + nb];
-                // plane_depth_at(cam, nb_plane, nb_centroid, centroid) (geometry.hpp:85-92)
-                const double ax = np.x * nr.x, ay = np.x * nr.y, az = np.x;
-                const double denom = (np.y * crs.x + np.z * crs.y) + np.w;
+    const int pitch = w.pitch;
+    for (int t0 = 0; t0 < N; t0 += 32) {
+        const int nr = min(32, N - t0);
+        double photo_sum = 0, vis_sum = 0;
+        int x_count = 0;
+        bool y_nonempty = false;
+        for (int b = 0; b < n; b += 32) {
+            const int i = b + lane;
+            bool ok = false;
+            double sv0 = 0, sv1 = 0, sv2 = 0;
+            if (i < n) {
+                const double2 r = mr[i];
+                const double denom = (p.y * r.x + p.z * r.y) + p.w;
                 if (!(fabs(denom) <= 1e-9)) {
-                    const double d = ((np.y * ax + np.z * ay) + np.w * az) / denom;
-                    if (d > 0 && !(d < a.d_min || d > a.d_max)) {
+                    const double s = plane_num / denom;
+                    if (s > 0) {
                         ok = true;
-                        cand = make_double4(d, np.y, np.z, np.w);
+                        sv0 = s * r.x;
+                        sv1 = s * r.y;
+                        sv2 = s;
                     }
                 }
             }
-        }
-        // ordered block compaction
-        s.scan[tid] = ok ? 1 : 0;
-        __syncthreads();
-        for (int off = 1; off < kThreads; off <<= 1) {
-            const int t = tid >= off ? s.scan[tid - off] : 0;
-            __syncthreads();
-            s.scan[tid] += t;
-            __syncthreads();
-        }
-        if (ok) s.cand[base + s.scan[tid] - 1] = cand;
-        base += s.scan[kThreads - 1];
-        __syncthreads();
-    }
-    if (tid == 0) s.n_cand = base;
-    __syncthreads();
-    if (a.use_s)
-        for (int i = tid; i < base; i += kThreads) s.es[i] = smoothness(a, v, sp, s.cand[i]);
-    __syncthreads();
-    run_candidates(a, s, v, sp, false);
-
-    // ---- phase B: normal_candidates (refine.hpp:213-242) at the current depth
-    bool okn = false;
-    double4 nc = make_double4(0, 0, 0, 0);
-    const double cur_depth = s.current.x;
-    if (tid < 8) {
-        const int k = tid;
-        const int ax_ = gx + kDir[k][0], ay_ = gy + kDir[k][1];
-        const int bx_ = gx + kDir[(k + 1) % 8][0], by_ = gy + kDir[(k + 1) % 8][1];
-        const bool ina = ax_ >= 0 && ay_ >= 0 && ax_ < a.gw && ay_ < a.gh;
-        const bool inb = bx_ >= 0 && by_ >= 0 && bx_ < a.gw && by_ < a.gh;
-        if (ina && inb) {
-            const int ia = ay_ * a.gw + ax_, ib = by_ * a.gw + bx_;
-            const double dr = cur0.x;  // snapshot depth of the reference superpixel
-            const double rx = dr * crs.x, ry = dr * crs.y, rz = dr;
-            const double da = a.planes[vs + ia].x, db = a.planes[vs + ib].x;
-            const double2 ra = a.cray[vs + ia], rb = a.cray[vs + ib];
-            const double A0 = da * ra.x - rx, A1 = da * ra.y - ry, A2 = da - rz;
-            const double B0 = db * rb.x - rx, B1 = db * rb.y - ry, B2 = db - rz;
-            double n0 = A1 * B2 - A2 * B1, n1 = A2 * B0 - A0 * B2, n2 = A0 * B1 - A1 * B0;
-            const double len = sqrt((n0 * n0 + n1 * n1) + n2 * n2);
-            if (!(len <= 1e-12)) {
-                n0 = n0 / len;
-                n1 = n1 / len;
-                n2 = n2 / len;
-                if ((n0 * crs.x + n1 * crs.y) + n2 > 0) {
-                    n0 = -n0;
-                    n1 = -n1;
-                    n2 = -n2;
+#pragma unroll 2
+            for (int tt = 0; tt < nr; ++tt) {
+                const int ti = t0 + tt;
+                double ph = -1.0, vsv = -2.0;
+                if (ok) {
+                    const double* rel = a.rel + ((size_t)v * N + ti) * 12;
+                    double x0, x1, x2;
+                    if (kIdR) {
+                        x0 = sv0 + rel[9];
+                        x1 = sv1 + rel[10];
+                        x2 = sv2 + rel[11];
+                    } else {
+                        x0 = ((rel[0] * sv0 + rel[1] * sv1) + rel[2] * sv2) + rel[9];
+                        x1 = ((rel[3] * sv0 + rel[4] * sv1) + rel[5] * sv2) + rel[10];
+                        x2 = ((rel[6] * sv0 + rel[7] * sv1) + rel[8] * sv2) + rel[11];
+                    }
+                    if (x2 > 0) {
+                        const int t = a.targets[(size_t)v * N + ti];
+                        const Cam& tc = a.cams[t];
+                        const double hx = kCanonK ? tc.K[0] * x0 + tc.K[2] * x2 : (tc.K[0] * x0 + tc.K[1] * x1) + tc.K[2] * x2;
+                        const double hy = tc.K[4] * x1 + tc.K[5] * x2;
+                        const double inv_z = 1.0 / x2;
+                        int px, py;
+                        if (!fast_lround(hx * inv_z, px)) px = lround_int(hx / x2);
+                        if (!fast_lround(hy * inv_z, py)) py = lround_int(hy / x2);
+                        if (!(px < 0 || py < 0 || px >= a.W || py >= a.H)) {
+                            const size_t q = (size_t)t * hw + (size_t)py * a.W + px;
+                            const int tlab = a.labels[q];
+                            const float4 c = a.color[(size_t)t * a.nsp + tlab];
+                            ph = libm::exp(-(double)color_dist2(rc.x, rc.y, rc.z, c.x, c.y, c.z) * a.inv_two_alpha2);
+                            const float td = a.depth[q];
+                            if (td > 0) {
+                                if (x2 <= (double)td * (1.0 + 1e-6)) {
+                                    const double rr = inv_z - 1.0 / (double)td;
+                                    vsv = libm::exp(-rr * rr * a.inv_two_sigma2);
+                                } else {
+                                    vsv = -1.0;
+                                }
+                            }
+                        }
+                    }
                 }
-                if (!((n0 * crs.x + n1 * crs.y) + n2 >= 0)) {
-                    if (!(cur_depth < a.d_min || cur_depth > a.d_max)) {
-                        okn = true;
-                        nc = make_double4(cur_depth, n0, n1, n2);
+                w.ph[lane * pitch + tt] = ph;
+                w.vs[lane * pitch + tt] = vsv;
+            }
+            __syncwarp();
+            if (lane < nr) {
+                const int nb = min(32, n - b);
+                for (int j = 0; j < nb; ++j) {
+                    const double ph = w.ph[j * pitch + lane];
+                    const double vsv = w.vs[j * pitch + lane];
+                    if (ph >= 0) photo_sum += ph;
+                    if (vsv >= 0) {
+                        vis_sum += vsv;
+                        ++x_count;
+                    } else if (vsv == -1.0) {
+                        y_nonempty = true;
                     }
                 }
             }
+            __syncwarp();
+        }
+        if (lane < nr) {
+            const double photo = photo_sum / (double)n;
+            const double vis = x_count > 0 ? photo * (vis_sum / x_count) : 0.0;
+            double occ = 0.0;
+            if (a.use_o && y_nonempty) occ = a.eta * (1.0 - (double)a.min_nb_sim[(size_t)v * a.nsp + sp]);
+            w.res[t0 + lane] = vis + occ;
         }
     }
-    s.scan[tid] = okn ? 1 : 0;
-    __syncthreads();
-    if (tid == 0) {
-        int acc = 0;
-        for (int k = 0; k < 8; ++k) {
-            const int t = s.scan[k];
-            s.scan[k] = acc;
-            acc += t;
-        }
-        s.n_cand = acc;
-    }
-    __syncthreads();
-    if (okn) s.cand[s.scan[tid]] = nc;
-    __syncthreads();
-    if (a.use_s && tid < s.n_cand) s.es[tid] = smoothness(a, v, sp, s.cand[tid]);
-    __syncthreads();
-    run_candidates(a, s, v, sp, false);
+    __syncwarp();
+    double acc = 0;
+    for (int t = 0; t < N; ++t) acc += w.res[t];
+    __syncwarp();
+    return acc / (double)N;
+}
 
-    if (tid == 0) {
-        a.out[vs + sp] = s.current;
-        if (s.accepted) atomicAdd(&a.counters[0], (unsigned long long)s.accepted);
+// The reference's sequential greedy over cand[0, n) (refine.hpp:279-303), candidate by
+// candidate in index order with the running prune E_s (1 + eta) <= e_cur: the same
+// candidates are evaluated as in the reference.  init: cand[0] is the current plane and its
+// energy initialises e_cur (refine.hpp:277).
+template <bool kIdR, bool kCanonK>
+__device__ __forceinline__ void greedy(const RefineArgs& a, const WarpSmem& w, int n, int v, int sp, int m0, int n_members,
+                       bool init, double& e_cur, double4& current, unsigned& accepted,
+                       unsigned long long& pix_evals, unsigned& cand_evals) {
+    const int lane = threadIdx.x & 31;
+    const bool prune = a.use_s && a.use_c;
+    int next = 0;
+    while (next < n) {
+        // next candidate that survives the prune test (ordered ballot scan)
+        const int idx = next + lane;
+        const bool pass = idx < n && (init || !prune || w.es[idx] * a.max_consistency > e_cur);
+        const unsigned m = __ballot_sync(LFDG_FULL_MASK, pass);
+        if (!m) {
+            next += 32;
+            continue;
+        }
+        const int c = next + __ffs(m) - 1;
+        next = c + 1;
+        const double4 cand = w.cand[c];
+        double e;
+        if (a.use_c) {
+            const double ec = consistency_warp<kIdR, kCanonK>(a, w, v, sp, cand, m0, n_members);
+            e = prune ? w.es[c] * ec : (a.use_s ? 1.0 * w.es[c] : 1.0) * ec;
+            pix_evals += (unsigned long long)a.N * n_members;
+        } else {
+            e = a.use_s ? 1.0 * w.es[c] : 1.0;
+        }
+        cand_evals++;
+        if (init) {
+            e_cur = e;
+        } else if (e > e_cur) {
+            e_cur = e;
+            current = cand;
+            accepted++;
+        }
+    }
+    __syncwarp();
+}
+
+// es of cand[0, n): 4 candidates per warp step (8 ring lanes each).
+__device__ void smoothness_all(const RefineArgs& a, const WarpSmem& w, int n, int v, int sp) {
+    const int lane = threadIdx.x & 31;
+    for (int b = 0; b < n; b += 4) {
+        const int ci = b + (lane >> 3);
+        const bool active = ci < n;
+        const double4 p = active ? w.cand[ci] : make_double4(1, 0, 0, -1);
+        const double es = smoothness_group(a, v, sp, p, active);
+        if (active && (lane & 7) == 0) w.es[ci] = es;
+    }
+    __syncwarp();
+}
+
+// Persistent kernel: each warp pulls (view, superpixel) tasks from a global counter and runs
+// refine_iteration's task body (refine.hpp:269-320) for it.
+template <bool kIdR, bool kCanonK>
+__global__ void __launch_bounds__(128) k_refine(RefineArgs a, int n_tasks, int* task_counter, int cap,
+                                                double4* g_cand, double* g_es) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int gwarp = blockIdx.x * 4 + warp;
+    unsigned char* base = smem_raw + warp * warp_smem_bytes(a.N);
+    WarpSmem w;
+    w.pitch = tile_pitch(a.N);
+    w.ph = reinterpret_cast<double*>(base);
+    w.vs = w.ph + 32 * w.pitch;
+    w.res = w.vs + 32 * w.pitch;
+    w.cand = g_cand + (size_t)gwarp * cap;
+    w.es = g_es + (size_t)gwarp * cap;
+
+    unsigned long long pix_evals = 0;
+    unsigned cand_evals = 0;
+    unsigned long long accepted_total = 0;
+    while (true) {
+        int task = 0;
+        if (lane == 0) task = atomicAdd(task_counter, 1);
+        task = __shfl_sync(LFDG_FULL_MASK, task, 0);
+        if (task >= n_tasks) break;
+        const int v = a.rv0 + task / a.nsp;
+        const int sp = task % a.nsp;
+        const size_t vs = (size_t)v * a.nsp;
+        const double4 cur0 = a.planes[vs + sp];
+        const int m0 = a.moff[(size_t)v * (a.nsp + 1) + sp];
+        const int n_members = a.moff[(size_t)v * (a.nsp + 1) + sp + 1] - m0;
+        double4 current = cur0;
+        double e_cur = 0;
+        unsigned accepted = 0;
+
+        // ---- e_cur = energy(current) (refine.hpp:277)
+        if (lane == 0) w.cand[0] = cur0;
+        __syncwarp();
+        if (a.use_s) smoothness_all(a, w, 1, v, sp);
+        greedy<kIdR, kCanonK>(a, w, 1, v, sp, m0, n_members, true, e_cur, current, accepted, pix_evals, cand_evals);
+
+        // ---- phase A: grid_neighbors(Kernel) order (superpixel.hpp:318-343), re-anchored
+        const int gx = sp % a.gw, gy = sp / a.gw;
+        const double2 crs = a.cray[vs + sp];
+        int n_cand = 0;
+        for (int s0 = 0; s0 < a.n_slots; s0 += 32) {
+            const int slot = s0 + lane;
+            bool ok = false;
+            double4 cand = make_double4(0, 0, 0, 0);
+            if (slot < a.n_slots) {
+                int dx, dy;
+                if (slot < 8) {
+                    dx = kDir[slot][0];
+                    dy = kDir[slot][1];
+                } else {
+                    const int k = (slot - 8) / a.per_dir;
+                    const int r = a.kernel_step * ((slot - 8) % a.per_dir + 1);
+                    dx = kDir[k][0] * r;
+                    dy = kDir[k][1] * r;
+                    if (abs(dx) <= 1 && abs(dy) <= 1) dx = 1 << 20;  // already in the ring
+                }
+                const int nx = gx + dx, ny = gy + dy;
+                if (nx >= 0 && ny >= 0 && nx < a.gw && ny < a.gh) {
+                    const int nb = ny * a.gw + nx;
+                    const double4 np = a.planes[vs + nb];
+                    const double2 nr = a.cray[vs + nb];
+                    // plane_depth_at(cam, nb_plane, nb_centroid, centroid) (geometry.hpp:85-92)
+                    const double ax = np.x * nr.x, ay = np.x * nr.y, az = np.x;
+                    const double denom = (np.y * crs.x + np.z * crs.y) + np.w;
+                    if (!(fabs(denom) <= 1e-9)) {
+                        const double d = ((np.y * ax + np.z * ay) + np.w * az) / denom;
+                        if (d > 0 && !(d < a.d_min || d > a.d_max)) {
+                            ok = true;
+                            cand = make_double4(d, np.y, np.z, np.w);
+                        }
+                    }
+                }
+            }
+            const unsigned m = __ballot_sync(LFDG_FULL_MASK, ok);
+            if (ok) w.cand[n_cand + __popc(m & ((1u << lane) - 1u))] = cand;
+            n_cand += __popc(m);
+        }
+        __syncwarp();
+        if (a.use_s) smoothness_all(a, w, n_cand, v, sp);
+        greedy<kIdR, kCanonK>(a, w, n_cand, v, sp, m0, n_members, false, e_cur, current, accepted, pix_evals, cand_evals);
+
+        // ---- phase B: normal_candidates (refine.hpp:213-242) at the phase-A depth
+        {
+            bool okn = false;
+            double4 nc = make_double4(0, 0, 0, 0);
+            const double cur_depth = current.x;
+            if (lane < 8) {
+                const int k = lane;
+                const int ax_ = gx + kDir[k][0], ay_ = gy + kDir[k][1];
+                const int bx_ = gx + kDir[(k + 1) & 7][0], by_ = gy + kDir[(k + 1) & 7][1];
+                const bool ina = ax_ >= 0 && ay_ >= 0 && ax_ < a.gw && ay_ < a.gh;
+                const bool inb = bx_ >= 0 && by_ >= 0 && bx_ < a.gw && by_ < a.gh;
+                if (ina && inb) {
+                    const int ia = ay_ * a.gw + ax_, ib = by_ * a.gw + bx_;
+                    const double dr = cur0.x;  // snapshot depth of this superpixel
+                    const double rx = dr * crs.x, ry = dr * crs.y, rz = dr;
+                    const double da = a.planes[vs + ia].x, db = a.planes[vs + ib].x;
+                    const double2 ra = a.cray[vs + ia], rb = a.cray[vs + ib];
+                    const double A0 = da * ra.x - rx, A1 = da * ra.y - ry, A2 = da - rz;
+                    const double B0 = db * rb.x - rx, B1 = db * rb.y - ry, B2 = db - rz;
+                    double n0 = A1 * B2 - A2 * B1, n1 = A2 * B0 - A0 * B2, n2 = A0 * B1 - A1 * B0;
+                    const double len = sqrt((n0 * n0 + n1 * n1) + n2 * n2);
+                    if (!(len <= 1e-12)) {
+                        n0 = n0 / len;
+                        n1 = n1 / len;
+                        n2 = n2 / len;
+                        if ((n0 * crs.x + n1 * crs.y) + n2 > 0) {
+                            n0 = -n0;
+                            n1 = -n1;
+                            n2 = -n2;
+                        }
+                        if (!((n0 * crs.x + n1 * crs.y) + n2 >= 0) && !(cur_depth < a.d_min || cur_depth > a.d_max)) {
+                            okn = true;
+                            nc = make_double4(cur_depth, n0, n1, n2);
+                        }
+                    }
+                }
+            }
+            const unsigned m = __ballot_sync(LFDG_FULL_MASK, okn);
+            if (okn) w.cand[__popc(m & ((1u << lane) - 1u))] = nc;
+            __syncwarp();
+            const int nn = __popc(m);
+            if (a.use_s) smoothness_all(a, w, nn, v, sp);
+            greedy<kIdR, kCanonK>(a, w, nn, v, sp, m0, n_members, false, e_cur, current, accepted, pix_evals, cand_evals);
+        }
+        if (lane == 0) a.out[vs + sp] = current;
+        accepted_total += accepted;
+        __syncwarp();
+    }
+    if (lane == 0) {
+        if (accepted_total) atomicAdd(&a.counters[0], accepted_total);
+        atomicAdd(&a.counters[2], pix_evals);
+        atomicAdd(&a.counters[3], (unsigned long long)cand_evals);
     }
 }
 
@@ -427,6 +507,9 @@ inline unsigned ceil_div(size_t a, size_t b) { return (unsigned)((a + b - 1) / b
 
 struct RefineDev {
     DevBuf<double2> mray;
+    DevBuf<int> task_counter;
+    DevBuf<double4> cand;
+    DevBuf<double> es;
 };
 RefineDev& refine_dev() {
     static RefineDev d;
@@ -535,10 +618,31 @@ void refine_iteration(Ctx& c, int l) {
     a.per_dir = a.radius_sp >= a.kernel_step ? a.radius_sp / a.kernel_step : 0;
     a.n_slots = 8 + 8 * a.per_dir;
     a.counters = c.counters.p;
-    if (a.n_slots + 8 > kMaxCand) throw Error(LFDG_INVALID_PARAMS, "propagation kernel too large for the device task");
-    if (a.N > kThreads) throw Error(LFDG_INVALID_PARAMS, "too many matching views for one CTA (max 128)");
+    if (a.N > kResCap) throw Error(LFDG_INVALID_PARAMS, "too many matching views (max 128)");
+    const int cap = std::max(a.n_slots, 8) + 1;
+    const size_t smem = 4 * warp_smem_bytes(a.N);
     if (rn > 0) {
-        k_refine<<<(unsigned)(rn * c.nsp), kThreads, 0, c.stream>>>(a);
+        auto launch = [&](auto kernel) {
+            LFDG_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            int per_sm = 0;
+            LFDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 128, smem));
+            const int n_tasks = rn * c.nsp;
+            const int blocks = std::max(1, std::min(per_sm * c.sm_count, (n_tasks + 3) / 4));
+            RefineDev& rd = refine_dev();
+            rd.task_counter.alloc(1);
+            rd.cand.alloc((size_t)blocks * 4 * cap);
+            rd.es.alloc((size_t)blocks * 4 * cap);
+            LFDG_CUDA_CHECK(cudaMemsetAsync(rd.task_counter.p, 0, sizeof(int), c.stream));
+            kernel<<<blocks, 128, smem, c.stream>>>(a, n_tasks, rd.task_counter.p, cap, rd.cand.p, rd.es.p);
+        };
+        if (c.identity_rot && c.canonical_k)
+            launch(k_refine<true, true>);
+        else if (c.identity_rot)
+            launch(k_refine<true, false>);
+        else if (c.canonical_k)
+            launch(k_refine<false, true>);
+        else
+            launch(k_refine<false, false>);
         LFDG_LAUNCHED(&c);
         LFDG_CUDA_CHECK(cudaMemcpyAsync(c.planes.p + (size_t)rv0 * c.nsp, c.planes_next.p + (size_t)rv0 * c.nsp,
                                         (size_t)rn * c.nsp * sizeof(double4), cudaMemcpyDeviceToDevice, c.stream));

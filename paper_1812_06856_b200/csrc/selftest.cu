@@ -36,3 +36,49 @@ extern "C" {
 int lfdg_selftest_exp(int device, const double* in, double* out, size_t n) { return run(device, in, out, n, k_exp); }
 int lfdg_selftest_expf(int device, const float* in, float* out, size_t n) { return run(device, in, out, n, k_expf); }
 }
+
+// FP64 roofline denominator: dependent-free DFMA stream (8 independent chains per thread,
+// grid = 148 SMs x 8 CTAs x 256 threads); returns achieved FLOP/s counting a DFMA as 2.
+namespace {
+__global__ void k_dfma(double* out, int iters, double a, double b) {
+    double x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+    for (int i = 0; i < iters; ++i) {
+        x0 = __fma_rn(x0, a, b); x1 = __fma_rn(x1, a, b); x2 = __fma_rn(x2, a, b); x3 = __fma_rn(x3, a, b);
+        x4 = __fma_rn(x4, a, b); x5 = __fma_rn(x5, a, b); x6 = __fma_rn(x6, a, b); x7 = __fma_rn(x7, a, b);
+    }
+    const double s = ((x0 + x1) + (x2 + x3)) + ((x4 + x5) + (x6 + x7));
+    if (s == 1.2345) out[0] = s;
+}
+}  // namespace
+
+extern "C" int lfdg_selftest_fp64_peak(int device, double* flops) {
+    try {
+        LFDG_CUDA_CHECK(cudaSetDevice(device));
+        int sms = 0;
+        LFDG_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        double* out = nullptr;
+        LFDG_CUDA_CHECK(cudaMalloc(&out, sizeof(double)));
+        const int iters = 4096, blocks = sms * 8, threads = 256;
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        k_dfma<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);  // warm-up
+        float best = 1e30f;
+        for (int r = 0; r < 5; ++r) {
+            cudaEventRecord(e0);
+            k_dfma<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);
+            cudaEventRecord(e1);
+            LFDG_CUDA_CHECK(cudaEventSynchronize(e1));
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e0, e1);
+            best = ms < best ? ms : best;
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaFree(out);
+        *flops = 2.0 * 8.0 * iters * (double)blocks * threads / (best * 1e-3);
+        return LFDG_OK;
+    } catch (const lfdg::Error& e) {
+        return e.code;
+    }
+}

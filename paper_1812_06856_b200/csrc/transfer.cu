@@ -1,0 +1,77 @@
+// Host <-> device transfers of the end-to-end path: LAB images in ([V][H][W][3] float, ideally
+// pinned host memory), planes + depth rasters out.  Uploads go through a float3 staging
+// buffer and a repack kernel into the float4 layout the kernels gather from, so a pinned
+// source is one DMA per view (no host-side reformatting).
+#include "context.h"
+
+namespace lfdg {
+namespace {
+__global__ void k_repack(const float* __restrict__ src, float4* __restrict__ dst, size_t n) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = make_float4(src[3 * i], src[3 * i + 1], src[3 * i + 2], 0.f);
+}
+struct Staging {
+    DevBuf<float> buf;
+};
+Staging& staging() {
+    static Staging s;
+    return s;
+}
+}  // namespace
+
+void upload_images(Ctx& c, int v0, int n, const float* host) {
+    c.require_views();
+    if (v0 < 0 || n < 0 || v0 + n > c.V) throw Error(LFDG_STATE, "view range out of bounds");
+    if (n == 0) return;
+    const size_t hw = c.hw();
+    Staging& s = staging();
+    s.buf.alloc((size_t)c.V * hw * 3);
+    LFDG_CUDA_CHECK(cudaMemcpyAsync(s.buf.p, host, (size_t)n * hw * 3 * sizeof(float), cudaMemcpyHostToDevice, c.stream));
+    const size_t m = (size_t)n * hw;
+    k_repack<<<(unsigned)((m + 255) / 256), 256, 0, c.stream>>>(s.buf.p, c.lab.p + (size_t)v0 * hw, m);
+    LFDG_LAUNCHED(&c);
+}
+
+void download_results(Ctx& c, int v0, int n, lfdg_plane* planes, float* depth) {
+    c.require_views();
+    if (v0 < 0 || n < 0 || v0 + n > c.V) throw Error(LFDG_STATE, "view range out of bounds");
+    if (planes)
+        LFDG_CUDA_CHECK(cudaMemcpyAsync(planes, c.planes.p + (size_t)v0 * c.nsp, (size_t)n * c.nsp * sizeof(lfdg_plane),
+                                        cudaMemcpyDeviceToHost, c.stream));
+    if (depth)
+        LFDG_CUDA_CHECK(cudaMemcpyAsync(depth, c.depth.p + (size_t)v0 * c.hw(), (size_t)n * c.hw() * sizeof(float),
+                                        cudaMemcpyDeviceToHost, c.stream));
+}
+
+}  // namespace lfdg
+
+extern "C" {
+
+int lfdg_upload_images(lfdg_ctx* p, int v0, int n, const float* images) {
+    try {
+        auto* c = reinterpret_cast<lfdg::Ctx*>(p);
+        if (!c) throw lfdg::Error(LFDG_STATE, "null context");
+        LFDG_CUDA_CHECK(cudaSetDevice(c->device));
+        lfdg::upload_images(*c, v0, n, images);
+        return LFDG_OK;
+    } catch (const lfdg::Error& e) {
+        lfdg::set_last_error(e.what());
+        return e.code;
+    }
+}
+
+int lfdg_download_results(lfdg_ctx* p, int v0, int n, lfdg_plane* planes, float* depth, int sync) {
+    try {
+        auto* c = reinterpret_cast<lfdg::Ctx*>(p);
+        if (!c) throw lfdg::Error(LFDG_STATE, "null context");
+        LFDG_CUDA_CHECK(cudaSetDevice(c->device));
+        lfdg::download_results(*c, v0, n, planes, depth);
+        if (sync) LFDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        return LFDG_OK;
+    } catch (const lfdg::Error& e) {
+        lfdg::set_last_error(e.what());
+        return e.code;
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,158 @@
+"""Device-resident orchestration of the hot path (the segment / init / refine stages of
+run_pipeline, pipeline.hpp:272-397), single- or multi-GPU.
+
+Multi-GPU: one process per GPU; views are partitioned into contiguous blocks,
+source images are replicated, every rank segments / sweeps / refines only its own views, and
+the per-view products other ranks read are exchanged with torch.distributed (NCCL over NVLink):
+  * once after SLIC: label maps, superpixel records, member CSR and centroid rays;
+  * after the sweep and after every refine_iteration: the per-superpixel planes (32 B each).
+Every rank then rasterizes every view locally.  rasterize is deterministic and the refinement
+is a Jacobi update, so the result is bit-identical for any GPU count.  The exchanges are in
+place on the context's own all-view buffers (zero-copy tensors over the device pointers).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import List, Optional, Tuple
+
+import numpy as np
+
+from . import _native as N
+from .api import DeviceContext, EnergyParams, SlicParams, SweepParams
+
+GRID_BUFFERS = (N.BUF_LABELS, N.BUF_CX, N.BUF_CY, N.BUF_COLOR, N.BUF_COUNT, N.BUF_MOFF, N.BUF_MPIX, N.BUF_CRAY)
+
+
+@dataclass
+class HotPathConfig:
+    slic: SlicParams = field(default_factory=SlicParams)
+    sweep: SweepParams = field(default_factory=SweepParams)
+    energy: EnergyParams = field(default_factory=EnergyParams)
+    seed: int = 0
+
+
+def partition(n_views: int, world: int, rank: int) -> Tuple[int, int]:
+    """Contiguous block of views owned by `rank` (sizes differ by at most one)."""
+    v0 = n_views * rank // world
+    v1 = n_views * (rank + 1) // world
+    return v0, v1 - v0
+
+
+class _CudaArray:
+    """Minimal __cuda_array_interface__ over a raw device pointer (zero-copy torch view)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class HotPath:
+    """SLIC -> sweep -> rasterize -> make_refine_context -> iterations x (refine; rasterize)."""
+
+    def __init__(self, device: int, images: np.ndarray, cams: np.ndarray, d_range, cfg: HotPathConfig,
+                 group=None, use_torch_stream: bool = True):
+        self.cfg = cfg
+        self.ctx = DeviceContext(device)
+        self.V = images.shape[0]
+        self.group = group
+        if group is not None:
+            import torch.distributed as dist
+
+            self.world = dist.get_world_size(group)
+            self.rank = dist.get_rank(group)
+        else:
+            self.world, self.rank = 1, 0
+        self.v0, self.n = partition(self.V, self.world, self.rank)
+        self.stream = None
+        if use_torch_stream:
+            # A dedicated torch stream, made current, so CUDA events, NCCL collectives and the
+            # library's kernels are ordered on one non-default stream.
+            import torch
+
+            torch.cuda.set_device(device)
+            self.stream = torch.cuda.Stream(device=device)
+            torch.cuda.set_stream(self.stream)
+            self.ctx.set_stream(self.stream.cuda_stream)
+        self.ctx.set_views(images, cams, d_range)
+
+    # ---- exchange plumbing
+    def _tensor(self, which: int):
+        import torch
+
+        ptr, nbytes, stride = self.ctx.device_buffer(which)
+        return torch.as_tensor(_CudaArray(ptr, nbytes), device=f"cuda:{self.ctx.device}"), stride
+
+    def _allgather(self, which: int):
+        import torch.distributed as dist
+
+        t, stride = self._tensor(which)
+        if self.V % self.world == 0:
+            chunk = stride * (self.V // self.world)
+            dist.all_gather_into_tensor(t, t[self.rank * chunk:(self.rank + 1) * chunk], group=self.group)
+        else:
+            for r in range(self.world):
+                v0, n = partition(self.V, self.world, r)
+                if n:
+                    dist.broadcast(t[v0 * stride:(v0 + n) * stride], src=r, group=self.group)
+
+    def _exchange_grids(self):
+        if self.world == 1:
+            return
+        for which in GRID_BUFFERS:
+            self._allgather(which)
+        self.ctx.mark_views_ready(0, self.V, 1)
+
+    def _exchange_planes(self):
+        if self.world == 1:
+            return
+        self._allgather(N.BUF_PLANES)
+        self.ctx.mark_views_ready(0, self.V, 2)
+
+    # ---- the path
+    def run(self, with_stats: bool = False) -> dict:
+        c, cfg = self.ctx, self.cfg
+        c.slic_views(self.v0, self.n, cfg.slic)
+        self._exchange_grids()
+        c.sweep_views(self.v0, self.n, cfg.sweep, cfg.seed)
+        self._exchange_planes()
+        c.rasterize()
+        c.make_refine_context(cfg.energy, cfg.sweep.levels)
+        c.set_refine_views(self.v0, self.n)
+        accepted = 0
+        for l in range(1, cfg.energy.iterations + 1):
+            r = c.refine_iteration(l, with_stats=with_stats)
+            if r is not None:
+                accepted += r[0]
+            self._exchange_planes()
+            c.rasterize()
+        return {"accepted": accepted if with_stats else None}
+
+    # ---- end-to-end transfers
+    def upload(self, images_host: np.ndarray):
+        """Enqueue the H2D copy of every view's LAB image (replicated on every rank)."""
+        images_host = np.ascontiguousarray(images_host, np.float32)
+        N.check(N.lib().lfdg_upload_images(self.ctx.h, 0, self.V, N.ptr(images_host)))
+
+    def download(self, planes_host: Optional[np.ndarray], depth_host: Optional[np.ndarray], sync: bool = True):
+        """Enqueue the D2H copy of this rank's views' planes [n][nsp][4] and depth [n][H][W]."""
+        N.check(N.lib().lfdg_download_results(self.ctx.h, self.v0, self.n,
+                                              None if planes_host is None else N.ptr(planes_host),
+                                              None if depth_host is None else N.ptr(depth_host), int(sync)))
+
+    def close(self):
+        self.ctx.close()
+
+
+def estimate_depth(images: np.ndarray, cams: np.ndarray, d_range, cfg: HotPathConfig = HotPathConfig(),
+                   device: int = 0) -> Tuple[List[np.ndarray], np.ndarray]:
+    """One-shot public entry: LAB images [V][H][W][3] (host) -> (planes per view, depth [V][H][W])."""
+    hp = HotPath(device, images, cams, d_range, cfg, use_torch_stream=False)
+    try:
+        hp.run()
+        nsp = hp.ctx.grid_shape(0)[0] * hp.ctx.grid_shape(0)[1]
+        planes = np.zeros((hp.V, nsp, 4), np.float64)
+        depth = np.zeros(images.shape[:3], np.float32)
+        hp.download(planes, depth, sync=True)
+        return list(planes), depth
+    finally:
+        hp.close()
