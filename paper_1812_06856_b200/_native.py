@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liblfdg.so")
+LIB_PATH = os.environ.get("LFDG_LIB") or os.path.join(HERE, "liblfdg.so")  # override: A/B experiments
 
 LFDG_OK = 0
 LFDG_INVALID_PARAMS = 1

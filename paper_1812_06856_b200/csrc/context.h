@@ -43,20 +43,26 @@ struct Error : std::runtime_error {
         (ctx)->launches++;                          \
     } while (0)
 
+// Grow-only device buffer: re-allocation (which synchronizes the device) happens only when a
+// larger size is requested, so steady-state calls never allocate.
 template <typename T>
 struct DevBuf {
     T* p = nullptr;
-    size_t n = 0;
+    size_t n = 0;    // requested element count
+    size_t cap = 0;  // allocated element count
     void alloc(size_t count) {
-        if (count == n && p) return;
-        release();
-        if (count) LFDG_CUDA_CHECK(cudaMalloc(&p, count * sizeof(T)));
         n = count;
+        if (count <= cap && p) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        if (count) LFDG_CUDA_CHECK(cudaMalloc(&p, count * sizeof(T)));
+        cap = count;
     }
     void release() {
         if (p) cudaFree(p);
         p = nullptr;
-        n = 0;
+        n = cap = 0;
     }
     ~DevBuf() { release(); }
 };
@@ -101,6 +107,8 @@ struct Ctx {
     std::vector<char> planes_ready;
     DevBuf<double4> planes, planes_next;
     DevBuf<float> depth;
+    DevBuf<int> sweep_targets;  // [V][N] matching views of the last sweep
+    DevBuf<float4> tcd;  // [V][H*W] refine gather raster: (mean colour of the pixel's label, depth)
 
     // refinement
     RefineTables refine;

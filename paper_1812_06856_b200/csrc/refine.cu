@@ -40,6 +40,7 @@ struct RefineArgs {
     const double2* mray;    // [V][HW] member rays in CSR order
     const double4* planes;  // snapshot [V][nsp]
     const float* depth;     // snapshot [V][HW]
+    const float4* tcd;      // [V][HW] (mean colour of the pixel's superpixel, snapshot depth)
     double4* out;           // [V][nsp]
     // context tables
     const int* targets;     // [V][N]
@@ -132,35 +133,48 @@ __device__ __forceinline__ bool fast_lround(double q, int& out) {
 }
 
 // Per-warp shared-memory slice.  Candidate planes / upper bounds live in a per-warp global
-// scratch row (L1-resident); the pixel-term tiles are shared memory.
+// scratch row (L1-resident); the per-task target table and the pixel-term tile are shared.
+struct TargetRow {   // one matching view of the task (refine.hpp:116-118, 46-47)
+    double R[9];
+    double T[3];
+    double K00, K01, K02, K11, K12;
+    int t;
+    int pad;
+};
 struct WarpSmem {
     double4* cand;  // [cap]   (global scratch)
     double* es;     // [cap]   (global scratch)
-    double* ph;     // [32][pitch] photo term of (pixel j, target tt): weight, or -1 (no sample)
-    double* vs;     // [32][pitch] visibility term: Gaussian (visible), -1 (occluded), -2 (no target depth)
-    double* res;    // [kResCap] V + O per target
+    TargetRow* tg;  // [N]
+    double* ph;     // [16][pitch] photo term of (pixel j, target tt): weight, or -1 (no sample)
+    double* vs;     // [16][pitch] visibility term: Gaussian (visible), -1 (occluded), -2 (no target depth)
+    double* res;    // [N] V + O per target
     int pitch;
 };
-constexpr int kResCap = 128;
+constexpr int kMaxTargets = 64;
+constexpr int kPixBlock = 16;  // member pixels per tile (a half-warp each; the halves split the targets)
 
 __host__ __device__ inline int tile_pitch(int N) {
     const int nr = N < 32 ? N : 32;
-    return (nr & 1) ? nr : nr + 1;  // odd pitch: conflict-free column reads, 2-way row writes
+    return (nr & 1) ? nr : nr + 1;  // odd pitch: conflict-free column reads
 }
 __host__ __device__ inline size_t warp_smem_bytes(int N) {
-    const size_t b = 2 * 32 * (size_t)tile_pitch(N) * sizeof(double) + kResCap * sizeof(double);
+    const size_t b = (size_t)N * sizeof(TargetRow) + 2 * kPixBlock * (size_t)tile_pitch(N) * sizeof(double) +
+                     (size_t)N * sizeof(double);
     return (b + 127) & ~(size_t)127;
 }
 
 // consistency_term (refine.hpp:189-199) of plane p for task (v, sp), one warp.
-// Lanes own 32 consecutive member pixels at a time (coherent branches, coalesced ray loads,
-// neighbouring gathers) and loop over the targets; the per-(pixel, target) terms go to a
-// shared tile, then lane t folds target t's column in member order — the reference's
+// Each half-warp owns the same 16 consecutive member pixels (coherent branches, coalesced ray
+// loads, neighbouring gathers); the halves take alternate targets.  Per-(pixel, target) terms
+// go to a shared tile, then lane t folds target t's column in member order — the reference's
 // sequential photo_sum / vis_sum / x_count / y_nonempty of pair_stats (refine.hpp:127-163),
 // bit for bit.  Finally V + O are summed in target order (refine.hpp:193-198).
 template <bool kIdR, bool kCanonK>
-__device__ __forceinline__ double consistency_warp(const RefineArgs& a, const WarpSmem& w, int v, int sp, double4 p, int m0, int n) {
+__device__ __forceinline__ double consistency_warp(const RefineArgs& a, const WarpSmem& w, int v, int sp, double4 p,
+                                                   int m0, int n) {
     const int lane = threadIdx.x & 31;
+    const int j = lane & (kPixBlock - 1);
+    const int half = lane >> 4;
     const int N = a.N;
     if (N == 0) return 1.0;
     const size_t hw = (size_t)a.W * a.H;
@@ -175,8 +189,8 @@ __device__ __forceinline__ double consistency_warp(const RefineArgs& a, const Wa
         double photo_sum = 0, vis_sum = 0;
         int x_count = 0;
         bool y_nonempty = false;
-        for (int b = 0; b < n; b += 32) {
-            const int i = b + lane;
+        for (int b = 0; b < n; b += kPixBlock) {
+            const int i = b + j;
             bool ok = false;
             double sv0 = 0, sv1 = 0, sv2 = 0;
             if (i < n) {
@@ -192,37 +206,33 @@ __device__ __forceinline__ double consistency_warp(const RefineArgs& a, const Wa
                     }
                 }
             }
-#pragma unroll 2
-            for (int tt = 0; tt < nr; ++tt) {
-                const int ti = t0 + tt;
+            for (int tt = half; tt < nr; tt += 2) {
+                const TargetRow& g = w.tg[t0 + tt];
                 double ph = -1.0, vsv = -2.0;
                 if (ok) {
-                    const double* rel = a.rel + ((size_t)v * N + ti) * 12;
                     double x0, x1, x2;
                     if (kIdR) {
-                        x0 = sv0 + rel[9];
-                        x1 = sv1 + rel[10];
-                        x2 = sv2 + rel[11];
+                        x0 = sv0 + g.T[0];
+                        x1 = sv1 + g.T[1];
+                        x2 = sv2 + g.T[2];
                     } else {
-                        x0 = ((rel[0] * sv0 + rel[1] * sv1) + rel[2] * sv2) + rel[9];
-                        x1 = ((rel[3] * sv0 + rel[4] * sv1) + rel[5] * sv2) + rel[10];
-                        x2 = ((rel[6] * sv0 + rel[7] * sv1) + rel[8] * sv2) + rel[11];
+                        x0 = ((g.R[0] * sv0 + g.R[1] * sv1) + g.R[2] * sv2) + g.T[0];
+                        x1 = ((g.R[3] * sv0 + g.R[4] * sv1) + g.R[5] * sv2) + g.T[1];
+                        x2 = ((g.R[6] * sv0 + g.R[7] * sv1) + g.R[8] * sv2) + g.T[2];
                     }
                     if (x2 > 0) {
-                        const int t = a.targets[(size_t)v * N + ti];
-                        const Cam& tc = a.cams[t];
-                        const double hx = kCanonK ? tc.K[0] * x0 + tc.K[2] * x2 : (tc.K[0] * x0 + tc.K[1] * x1) + tc.K[2] * x2;
-                        const double hy = tc.K[4] * x1 + tc.K[5] * x2;
+                        const double hx = kCanonK ? g.K00 * x0 + g.K02 * x2 : (g.K00 * x0 + g.K01 * x1) + g.K02 * x2;
+                        const double hy = g.K11 * x1 + g.K12 * x2;
                         const double inv_z = 1.0 / x2;
                         int px, py;
                         if (!fast_lround(hx * inv_z, px)) px = lround_int(hx / x2);
                         if (!fast_lround(hy * inv_z, py)) py = lround_int(hy / x2);
                         if (!(px < 0 || py < 0 || px >= a.W || py >= a.H)) {
-                            const size_t q = (size_t)t * hw + (size_t)py * a.W + px;
-                            const int tlab = a.labels[q];
-                            const float4 c = a.color[(size_t)t * a.nsp + tlab];
+                            // tgrid.sp[tgrid.label(px, py)].mean_color and snapshot.depth[t](px, py)
+                            // (refine.hpp:146-152) in one 16-byte gather
+                            const float4 c = __ldg(&a.tcd[(size_t)g.t * hw + (size_t)py * a.W + px]);
                             ph = libm::exp(-(double)color_dist2(rc.x, rc.y, rc.z, c.x, c.y, c.z) * a.inv_two_alpha2);
-                            const float td = a.depth[q];
+                            const float td = c.w;
                             if (td > 0) {
                                 if (x2 <= (double)td * (1.0 + 1e-6)) {
                                     const double rr = inv_z - 1.0 / (double)td;
@@ -234,15 +244,15 @@ __device__ __forceinline__ double consistency_warp(const RefineArgs& a, const Wa
                         }
                     }
                 }
-                w.ph[lane * pitch + tt] = ph;
-                w.vs[lane * pitch + tt] = vsv;
+                w.ph[j * pitch + tt] = ph;
+                w.vs[j * pitch + tt] = vsv;
             }
             __syncwarp();
             if (lane < nr) {
-                const int nb = min(32, n - b);
-                for (int j = 0; j < nb; ++j) {
-                    const double ph = w.ph[j * pitch + lane];
-                    const double vsv = w.vs[j * pitch + lane];
+                const int nb = min(kPixBlock, n - b);
+                for (int jj = 0; jj < nb; ++jj) {
+                    const double ph = w.ph[jj * pitch + lane];
+                    const double vsv = w.vs[jj * pitch + lane];
                     if (ph >= 0) photo_sum += ph;
                     if (vsv >= 0) {
                         vis_sum += vsv;
@@ -337,9 +347,10 @@ __global__ void __launch_bounds__(128) k_refine(RefineArgs a, int n_tasks, int* 
     unsigned char* base = smem_raw + warp * warp_smem_bytes(a.N);
     WarpSmem w;
     w.pitch = tile_pitch(a.N);
-    w.ph = reinterpret_cast<double*>(base);
-    w.vs = w.ph + 32 * w.pitch;
-    w.res = w.vs + 32 * w.pitch;
+    w.tg = reinterpret_cast<TargetRow*>(base);
+    w.ph = reinterpret_cast<double*>(base + (size_t)a.N * sizeof(TargetRow));
+    w.vs = w.ph + kPixBlock * w.pitch;
+    w.res = w.vs + kPixBlock * w.pitch;
     w.cand = g_cand + (size_t)gwarp * cap;
     w.es = g_es + (size_t)gwarp * cap;
 
@@ -360,6 +371,21 @@ __global__ void __launch_bounds__(128) k_refine(RefineArgs a, int n_tasks, int* 
         double4 current = cur0;
         double e_cur = 0;
         unsigned accepted = 0;
+        for (int ti = lane; ti < a.N; ti += 32) {  // the task's matching views (refine.hpp:116-118)
+            const int t = a.targets[(size_t)v * a.N + ti];
+            const double* rel = a.rel + ((size_t)v * a.N + ti) * 12;
+            TargetRow& g = w.tg[ti];
+            for (int k = 0; k < 9; ++k) g.R[k] = rel[k];
+            for (int k = 0; k < 3; ++k) g.T[k] = rel[9 + k];
+            const Cam& tc = a.cams[t];
+            g.K00 = tc.K[0];
+            g.K01 = tc.K[1];
+            g.K02 = tc.K[2];
+            g.K11 = tc.K[4];
+            g.K12 = tc.K[5];
+            g.t = t;
+        }
+        __syncwarp();
 
         // ---- e_cur = energy(current) (refine.hpp:277)
         if (lane == 0) w.cand[0] = cur0;
@@ -491,6 +517,17 @@ __global__ void k_color_tables(const float4* __restrict__ color, int nsp, int gw
     min_nb_sim[(size_t)v * nsp + sp] = m;
 }
 
+// tcd[v][p] = (mean colour of label(p), depth(p)) for every view.
+__global__ void k_build_tcd(const int32_t* __restrict__ labels, const float4* __restrict__ color,
+                            const float* __restrict__ depth, int W, int H, int nsp, float4* tcd) {
+    const size_t hw = (size_t)W * H;
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= hw) return;
+    const int v = blockIdx.y;
+    const float4 c = color[(size_t)v * nsp + labels[(size_t)v * hw + i]];
+    tcd[(size_t)v * hw + i] = make_float4(c.x, c.y, c.z, depth[(size_t)v * hw + i]);
+}
+
 // Member rays in CSR order: mray[v][k] = ray(pixel mpix[v][k]) (geometry.hpp:45).
 __global__ void k_member_rays(const int32_t* __restrict__ mpix, const Cam* cams, int W, int H, double2* mray) {
     const size_t hw = (size_t)W * H;
@@ -567,7 +604,7 @@ void make_refine_tables(Ctx& c, const lfdg_energy_params& p, int sweep_levels) {
     rd.mray.alloc((size_t)c.V * c.hw());
     k_member_rays<<<dim3(ceil_div(c.hw(), 256), c.V), 256, 0, st>>>(c.mpix.p, c.d_cams.p, c.W, c.H, rd.mray.p);
     LFDG_LAUNCHED(&c);
-    LFDG_CUDA_CHECK(cudaStreamSynchronize(st));
+    c.tcd.alloc((size_t)c.V * c.hw());
     t.ready = true;
 }
 
@@ -594,6 +631,7 @@ void refine_iteration(Ctx& c, int l) {
     a.mray = refine_dev().mray.p;
     a.planes = c.planes.p;
     a.depth = c.depth.p;
+    a.tcd = c.tcd.p;
     a.out = c.planes_next.p;
     a.targets = t.targets.p;
     a.rel = t.rel.p;
@@ -618,10 +656,14 @@ void refine_iteration(Ctx& c, int l) {
     a.per_dir = a.radius_sp >= a.kernel_step ? a.radius_sp / a.kernel_step : 0;
     a.n_slots = 8 + 8 * a.per_dir;
     a.counters = c.counters.p;
-    if (a.N > kResCap) throw Error(LFDG_INVALID_PARAMS, "too many matching views (max 128)");
+    if (a.N > kMaxTargets) throw Error(LFDG_INVALID_PARAMS, "too many matching views (max 64)");
     const int cap = std::max(a.n_slots, 8) + 1;
     const size_t smem = 4 * warp_smem_bytes(a.N);
     if (rn > 0) {
+        // the refine gather raster from the current snapshot (labels, colours, depth)
+        k_build_tcd<<<dim3(ceil_div(c.hw(), 256), c.V), 256, 0, c.stream>>>(c.labels.p, c.color.p, c.depth.p, c.W,
+                                                                             c.H, c.nsp, c.tcd.p);
+        LFDG_LAUNCHED(&c);
         auto launch = [&](auto kernel) {
             LFDG_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             int per_sm = 0;

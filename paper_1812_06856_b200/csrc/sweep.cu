@@ -100,6 +100,60 @@ __device__ __forceinline__ float sweep_sample(const Cam& rc, const Cam& tc, cons
     return d2 < T ? d2 : T;
 }
 
+// Bilinear TSSD of one mapped sample (image.hpp:47-67, sweep.hpp:32-34, :99-103).
+__device__ __forceinline__ float tssd_at(const float4* __restrict__ timg, int W, int H, double u, double v, float4 ref,
+                                         float T) {
+    if (!(u >= 0.0 && v >= 0.0 && u <= W - 1.0 && v <= H - 1.0)) return T;
+    int x0 = (int)floor(u);
+    int y0 = (int)floor(v);
+    if (x0 >= W - 1) x0 = W - 2;
+    if (y0 >= H - 1) y0 = H - 2;
+    if (x0 < 0) x0 = 0;
+    if (y0 < 0) y0 = 0;
+    const float fx = (float)(u - x0);
+    const float fy = (float)(v - y0);
+    const float4* r0 = timg + (y0 * W + x0);
+    const float4 p00 = __ldg(r0), p10 = __ldg(r0 + 1);
+    const float4 p01 = __ldg(r0 + W), p11 = __ldg(r0 + W + 1);
+    const float t0 = p00.x + fx * (p10.x - p00.x), b0 = p01.x + fx * (p11.x - p01.x);
+    const float t1 = p00.y + fx * (p10.y - p00.y), b1 = p01.y + fx * (p11.y - p01.y);
+    const float t2 = p00.z + fx * (p10.z - p00.z), b2 = p01.z + fx * (p11.z - p01.z);
+    const float d2 = color_dist2(ref.x, ref.y, ref.z, t0 + fy * (b0 - t0), t1 + fy * (b1 - t1), t2 + fy * (b2 - t2));
+    return d2 < T ? d2 : T;
+}
+
+// The kIdR && kCanonK inner loop over a staged chunk, for one (hypothesis, target).  With every
+// rotation exactly I, the target-frame z = (d - t_ref.z) + t_t.z is the same for every member
+// pixel, so h.z = z and K02 z, K12 z are hoisted, and u = hx / z, v = hy / z use z's correctly
+// rounded reciprocal plus one Markstein correction (q = hx rz; r = fma(-q, z, hx) exact;
+// q' = fma(r, rz, q)), which is the correctly rounded quotient for operands away from
+// overflow/underflow.  The cost chain is the reference's, sample by sample.
+__device__ __forceinline__ double sweep_chunk_fast(double cost, const double2* __restrict__ s_ray,
+                                                   const float4* __restrict__ s_ref, int cn,
+                                                   const float4* __restrict__ timg, int W, int H, double d,
+                                                   const Cam& rc, const Cam& tc, float T) {
+    const double rt0 = rc.t[0], rt1 = rc.t[1];
+    const double z = (d - rc.t[2]) + tc.t[2];
+    if (!(z > 0)) {
+        for (int i = 0; i < cn; ++i) cost += (double)T;
+        return cost;
+    }
+    const double tt0 = tc.t[0], tt1 = tc.t[1];
+    const double K00 = tc.K[0], K11 = tc.K[4];
+    const double Kz0 = tc.K[2] * z, Kz1 = tc.K[5] * z;
+    const double rz = 1.0 / z;
+    for (int i = 0; i < cn; ++i) {
+        const double2 ray = s_ray[i];
+        const double hx = K00 * ((d * ray.x - rt0) + tt0) + Kz0;
+        const double hy = K11 * ((d * ray.y - rt1) + tt1) + Kz1;
+        const double qx = hx * rz, qy = hy * rz;
+        const double u = __fma_rn(__fma_rn(-qx, z, hx), rz, qx);
+        const double v = __fma_rn(__fma_rn(-qy, z, hy), rz, qy);
+        cost += (double)tssd_at(timg, W, H, u, v, s_ref[i], T);
+    }
+    return cost;
+}
+
 template <bool kIdR, bool kCanonK>
 __global__ void __launch_bounds__(256) k_sweep(const float4* __restrict__ lab, int W, int H, int nsp, int v0,
                                                const Cam* __restrict__ cams, const int* __restrict__ targets,
@@ -166,6 +220,10 @@ __global__ void __launch_bounds__(256) k_sweep(const float4* __restrict__ lab, i
                 }
                 if (!active) continue;
                 const int cn = min(kSweepCap, n - c0);
+                if (kIdR && kCanonK) {
+                    cost = sweep_chunk_fast(cost, s_ray, s_ref, cn, timg, W, H, d, rc, tc, T);
+                    continue;
+                }
                 for (int i = 0; i < cn; ++i) {
                     const double2 ray = s_ray[i];
                     const float t = sweep_sample<kIdR, kCanonK>(rc, tc, timg, W, H, d, ray.x, ray.y, s_ref[i], T);
@@ -273,7 +331,7 @@ void sweep_views(Ctx& c, int v0, int n, const lfdg_sweep_params& p, uint64_t see
         const std::vector<int> t = matching_views(c, v, p.max_neighbors);
         for (int i = 0; i < nt; ++i) tg[(size_t)v * nt + i] = t[i];
     }
-    DevBuf<int> d_tg;
+    DevBuf<int>& d_tg = c.sweep_targets;
     d_tg.alloc(tg.size());
     LFDG_CUDA_CHECK(cudaMemcpyAsync(d_tg.p, tg.data(), tg.size() * sizeof(int), cudaMemcpyHostToDevice, c.stream));
     const double inv_lo = 1.0 / c.d_max;
@@ -297,8 +355,6 @@ void sweep_views(Ctx& c, int v0, int n, const lfdg_sweep_params& p, uint64_t see
     else
         launch(k_sweep<false, false>);
     LFDG_LAUNCHED(&c);
-    // d_tg is freed at scope exit; make sure the kernel has consumed it.
-    LFDG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
     for (int b = 0; b < n; ++b) c.planes_ready[v0 + b] = 1;
 }
 
