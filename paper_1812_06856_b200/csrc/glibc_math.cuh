@@ -92,8 +92,9 @@ LFDG_HD double fma_(double a, double b, double c) {
 #endif
 }
 
-// __exp_fma (glibc sysdeps/ieee754/dbl-64/e_exp.c, x86-64 FMA build).
-LFDG_HD double exp(double x) {
+// __exp_fma (glibc sysdeps/ieee754/dbl-64/e_exp.c, x86-64 FMA build).  `tab` (nullable) is a
+// copy of the 256-entry table, e.g. staged in shared memory by a hot kernel.
+LFDG_HD double exp_with(double x, const uint64_t* tab) {
     const double kInvLn2N = 0x1.71547652b82fep+7;
     const double kShift = 0x1.8p+52;
     const double kNegLn2hiN = -0x1.62e42fefa0000p-8;
@@ -118,8 +119,8 @@ LFDG_HD double exp(double x) {
     const double r = fma_(kd, kNegLn2loN, fma_(kd, kNegLn2hiN, x));
     const unsigned idx = 2u * (unsigned)(ki & 127u);
     const uint64_t top = ki << 45;
-    const double tail = as_f64(exp_tab(idx));
-    uint64_t sbits = exp_tab(idx + 1) + top;
+    const double tail = as_f64(tab ? tab[idx] : exp_tab(idx));
+    uint64_t sbits = (tab ? tab[idx + 1] : exp_tab(idx + 1)) + top;
     const double r2 = r * r;
     const double tmp = fma_(r2 * r2, fma_(r, C5, C4), fma_(fma_(r, C3, C2), r2, r + tail));
     if (abstop == 0) {
@@ -144,6 +145,16 @@ LFDG_HD double exp(double x) {
     const double scale = as_f64(sbits);
     return fma_(scale, tmp, scale);
 }
+
+LFDG_HD double exp(double x) { return exp_with(x, nullptr); }
+
+#if defined(__CUDACC__)
+// Copy the exp table into shared memory (block-cooperative); returns the smem pointer.
+__device__ __forceinline__ const uint64_t* stage_exp_table(uint64_t* smem256) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) smem256[i] = kExpTabDev[i];
+    return smem256;
+}
+#endif
 
 // __expf_fma (glibc sysdeps/ieee754/flt-32/e_expf.c, x86-64 FMA build).
 LFDG_HD float expf(float x) {

@@ -41,6 +41,7 @@ struct RefineArgs {
     const double4* planes;  // snapshot [V][nsp]
     const float* depth;     // snapshot [V][HW]
     const float4* tcd;      // [V][HW] (mean colour of the pixel's superpixel, snapshot depth)
+    const double2* tinv;    // [V][HW] (depth * (1 + 1e-6), 1 / depth) in f64 (refine.hpp:156-157)
     double4* out;           // [V][nsp]
     // context tables
     const int* targets;     // [V][N]
@@ -120,15 +121,17 @@ __device__ __forceinline__ double smoothness_group(const RefineArgs& a, int v, i
     return acc / wsum;
 }
 
-// lround(q) for q = hx / z computed as hx * (1/z): exact whenever q is farther than 8x the
-// product's error bound (2^-52 |q|) from a rounding boundary (a half-integer); otherwise the
-// caller falls back to the true division.  Returns false when the fast value cannot be used.
+// lround(u) for u = hx / z from q = hx * (1/z).  |q - u| <= 2^-52 |u| (two roundings), so when
+// q is farther than 8x that bound from a half-integer, u rounds to the same integer as q; the
+// nearest integer is read off the low word of q + 1.5*2^52 (round-to-nearest, no F2I).  Near a
+// half-integer (or |q| >= 2^30) it returns false and the caller divides exactly.
 __device__ __forceinline__ bool fast_lround(double q, int& out) {
     const double aq = fabs(q);
     if (!(aq < 0x1p30)) return false;
-    const double f = q - floor(q);
-    if (fabs(f - 0.5) <= aq * 0x1p-49 + 0x1p-1000) return false;
-    out = (int)llround(q);
+    const double t = q + 0x1.8p52;
+    const double d = q - (t - 0x1.8p52);  // exact, in [-0.5, 0.5]
+    if (fabs(d) >= 0.5 - (aq * 0x1p-49 + 0x1p-1000)) return false;
+    out = __double2loint(t);
     return true;
 }
 
@@ -148,6 +151,7 @@ struct WarpSmem {
     double* ph;     // [16][pitch] photo term of (pixel j, target tt): weight, or -1 (no sample)
     double* vs;     // [16][pitch] visibility term: Gaussian (visible), -1 (occluded), -2 (no target depth)
     double* res;    // [N] V + O per target
+    const uint64_t* exptab;  // glibc exp table staged in shared memory (per block)
     int pitch;
 };
 constexpr int kMaxTargets = 64;
@@ -231,12 +235,13 @@ __device__ __forceinline__ double consistency_warp(const RefineArgs& a, const Wa
                             // tgrid.sp[tgrid.label(px, py)].mean_color and snapshot.depth[t](px, py)
                             // (refine.hpp:146-152) in one 16-byte gather
                             const float4 c = __ldg(&a.tcd[(size_t)g.t * hw + (size_t)py * a.W + px]);
-                            ph = libm::exp(-(double)color_dist2(rc.x, rc.y, rc.z, c.x, c.y, c.z) * a.inv_two_alpha2);
+                            ph = libm::exp_with(-(double)color_dist2(rc.x, rc.y, rc.z, c.x, c.y, c.z) * a.inv_two_alpha2,
+                                                w.exptab);
                             const float td = c.w;
                             if (td > 0) {
                                 if (x2 <= (double)td * (1.0 + 1e-6)) {
                                     const double rr = inv_z - 1.0 / (double)td;
-                                    vsv = libm::exp(-rr * rr * a.inv_two_sigma2);
+                                    vsv = libm::exp_with(-rr * rr * a.inv_two_sigma2, w.exptab);
                                 } else {
                                     vsv = -1.0;
                                 }
@@ -338,12 +343,15 @@ __device__ void smoothness_all(const RefineArgs& a, const WarpSmem& w, int n, in
 // Persistent kernel: each warp pulls (view, superpixel) tasks from a global counter and runs
 // refine_iteration's task body (refine.hpp:269-320) for it.
 template <bool kIdR, bool kCanonK>
-__global__ void __launch_bounds__(128) k_refine(RefineArgs a, int n_tasks, int* task_counter, int cap,
+__global__ void __launch_bounds__(128, 8) k_refine(RefineArgs a, int n_tasks, int* task_counter, int cap,
                                                 double4* g_cand, double* g_es) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ uint64_t s_exptab[256];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int gwarp = blockIdx.x * 4 + warp;
+    libm::stage_exp_table(s_exptab);
+    __syncthreads();
     unsigned char* base = smem_raw + warp * warp_smem_bytes(a.N);
     WarpSmem w;
     w.pitch = tile_pitch(a.N);
@@ -351,6 +359,7 @@ __global__ void __launch_bounds__(128) k_refine(RefineArgs a, int n_tasks, int* 
     w.ph = reinterpret_cast<double*>(base + (size_t)a.N * sizeof(TargetRow));
     w.vs = w.ph + kPixBlock * w.pitch;
     w.res = w.vs + kPixBlock * w.pitch;
+    w.exptab = s_exptab;
     w.cand = g_cand + (size_t)gwarp * cap;
     w.es = g_es + (size_t)gwarp * cap;
 
@@ -362,8 +371,14 @@ __global__ void __launch_bounds__(128) k_refine(RefineArgs a, int n_tasks, int* 
         if (lane == 0) task = atomicAdd(task_counter, 1);
         task = __shfl_sync(LFDG_FULL_MASK, task, 0);
         if (task >= n_tasks) break;
-        const int v = a.rv0 + task / a.nsp;
-        const int sp = task % a.nsp;
+        // Task order (superpixel row, view, superpixel column): warps running concurrently work on
+        // the same band of image rows in every view, so the target gathers of all in-flight
+        // tasks share one L2-resident band instead of streaming whole views (L2 locality).
+        const int rn = n_tasks / a.nsp;
+        const int row = task / (rn * a.gw);
+        const int rem = task - row * rn * a.gw;
+        const int v = a.rv0 + rem / a.gw;
+        const int sp = row * a.gw + rem % a.gw;
         const size_t vs = (size_t)v * a.nsp;
         const double4 cur0 = a.planes[vs + sp];
         const int m0 = a.moff[(size_t)v * (a.nsp + 1) + sp];
@@ -517,15 +532,20 @@ __global__ void k_color_tables(const float4* __restrict__ color, int nsp, int gw
     min_nb_sim[(size_t)v * nsp + sp] = m;
 }
 
-// tcd[v][p] = (mean colour of label(p), depth(p)) for every view.
+// Refine gather rasters for every view: tcd[v][p] = (mean colour of label(p), depth(p)) and
+// tinv[v][p] = ((double)depth(p) * (1 + 1e-6), 1 / (double)depth(p)) — the target-side operands
+// of pair_stats (refine.hpp:146-158), computed once per snapshot with the reference's operations.
 __global__ void k_build_tcd(const int32_t* __restrict__ labels, const float4* __restrict__ color,
-                            const float* __restrict__ depth, int W, int H, int nsp, float4* tcd) {
+                            const float* __restrict__ depth, int W, int H, int nsp, float4* tcd, double2* tinv) {
     const size_t hw = (size_t)W * H;
     const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= hw) return;
     const int v = blockIdx.y;
     const float4 c = color[(size_t)v * nsp + labels[(size_t)v * hw + i]];
-    tcd[(size_t)v * hw + i] = make_float4(c.x, c.y, c.z, depth[(size_t)v * hw + i]);
+    const float td = depth[(size_t)v * hw + i];
+    tcd[(size_t)v * hw + i] = make_float4(c.x, c.y, c.z, td);
+    tinv[(size_t)v * hw + i] = td > 0 ? make_double2((double)td * (1.0 + 1e-6), 1.0 / (double)td)
+                                      : make_double2(0.0, 0.0);
 }
 
 // Member rays in CSR order: mray[v][k] = ray(pixel mpix[v][k]) (geometry.hpp:45).
@@ -605,6 +625,7 @@ void make_refine_tables(Ctx& c, const lfdg_energy_params& p, int sweep_levels) {
     k_member_rays<<<dim3(ceil_div(c.hw(), 256), c.V), 256, 0, st>>>(c.mpix.p, c.d_cams.p, c.W, c.H, rd.mray.p);
     LFDG_LAUNCHED(&c);
     c.tcd.alloc((size_t)c.V * c.hw());
+    c.tinv.alloc((size_t)c.V * c.hw());
     t.ready = true;
 }
 
@@ -632,6 +653,7 @@ void refine_iteration(Ctx& c, int l) {
     a.planes = c.planes.p;
     a.depth = c.depth.p;
     a.tcd = c.tcd.p;
+    a.tinv = c.tinv.p;
     a.out = c.planes_next.p;
     a.targets = t.targets.p;
     a.rel = t.rel.p;
@@ -662,7 +684,7 @@ void refine_iteration(Ctx& c, int l) {
     if (rn > 0) {
         // the refine gather raster from the current snapshot (labels, colours, depth)
         k_build_tcd<<<dim3(ceil_div(c.hw(), 256), c.V), 256, 0, c.stream>>>(c.labels.p, c.color.p, c.depth.p, c.W,
-                                                                             c.H, c.nsp, c.tcd.p);
+                                                                             c.H, c.nsp, c.tcd.p, c.tinv.p);
         LFDG_LAUNCHED(&c);
         auto launch = [&](auto kernel) {
             LFDG_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
