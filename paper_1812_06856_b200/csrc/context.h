@@ -109,7 +109,6 @@ struct Ctx {
     DevBuf<float> depth;
     DevBuf<int> sweep_targets;  // [V][N] matching views of the last sweep
     DevBuf<float4> tcd;  // [V][H*W] refine gather raster: (mean colour of the pixel's label, depth)
-    DevBuf<double2> tinv;  // [V][H*W] refine gather raster: (depth (1 + 1e-6), 1 / depth) in f64
 
     // refinement
     RefineTables refine;

@@ -41,7 +41,6 @@ struct RefineArgs {
     const double4* planes;  // snapshot [V][nsp]
     const float* depth;     // snapshot [V][HW]
     const float4* tcd;      // [V][HW] (mean colour of the pixel's superpixel, snapshot depth)
-    const double2* tinv;    // [V][HW] (depth * (1 + 1e-6), 1 / depth) in f64 (refine.hpp:156-157)
     double4* out;           // [V][nsp]
     // context tables
     const int* targets;     // [V][N]
@@ -532,11 +531,10 @@ __global__ void k_color_tables(const float4* __restrict__ color, int nsp, int gw
     min_nb_sim[(size_t)v * nsp + sp] = m;
 }
 
-// Refine gather rasters for every view: tcd[v][p] = (mean colour of label(p), depth(p)) and
-// tinv[v][p] = ((double)depth(p) * (1 + 1e-6), 1 / (double)depth(p)) — the target-side operands
-// of pair_stats (refine.hpp:146-158), computed once per snapshot with the reference's operations.
+// Refine gather raster for every view: tcd[v][p] = (mean colour of label(p), depth(p)), the
+// target-side operands of pair_stats (refine.hpp:146-152) in one 16-byte record per pixel.
 __global__ void k_build_tcd(const int32_t* __restrict__ labels, const float4* __restrict__ color,
-                            const float* __restrict__ depth, int W, int H, int nsp, float4* tcd, double2* tinv) {
+                            const float* __restrict__ depth, int W, int H, int nsp, float4* tcd) {
     const size_t hw = (size_t)W * H;
     const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= hw) return;
@@ -544,8 +542,6 @@ __global__ void k_build_tcd(const int32_t* __restrict__ labels, const float4* __
     const float4 c = color[(size_t)v * nsp + labels[(size_t)v * hw + i]];
     const float td = depth[(size_t)v * hw + i];
     tcd[(size_t)v * hw + i] = make_float4(c.x, c.y, c.z, td);
-    tinv[(size_t)v * hw + i] = td > 0 ? make_double2((double)td * (1.0 + 1e-6), 1.0 / (double)td)
-                                      : make_double2(0.0, 0.0);
 }
 
 // Member rays in CSR order: mray[v][k] = ray(pixel mpix[v][k]) (geometry.hpp:45).
@@ -625,7 +621,6 @@ void make_refine_tables(Ctx& c, const lfdg_energy_params& p, int sweep_levels) {
     k_member_rays<<<dim3(ceil_div(c.hw(), 256), c.V), 256, 0, st>>>(c.mpix.p, c.d_cams.p, c.W, c.H, rd.mray.p);
     LFDG_LAUNCHED(&c);
     c.tcd.alloc((size_t)c.V * c.hw());
-    c.tinv.alloc((size_t)c.V * c.hw());
     t.ready = true;
 }
 
@@ -653,7 +648,6 @@ void refine_iteration(Ctx& c, int l) {
     a.planes = c.planes.p;
     a.depth = c.depth.p;
     a.tcd = c.tcd.p;
-    a.tinv = c.tinv.p;
     a.out = c.planes_next.p;
     a.targets = t.targets.p;
     a.rel = t.rel.p;
@@ -684,7 +678,7 @@ void refine_iteration(Ctx& c, int l) {
     if (rn > 0) {
         // the refine gather raster from the current snapshot (labels, colours, depth)
         k_build_tcd<<<dim3(ceil_div(c.hw(), 256), c.V), 256, 0, c.stream>>>(c.labels.p, c.color.p, c.depth.p, c.W,
-                                                                             c.H, c.nsp, c.tcd.p, c.tinv.p);
+                                                                             c.H, c.nsp, c.tcd.p);
         LFDG_LAUNCHED(&c);
         auto launch = [&](auto kernel) {
             LFDG_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
