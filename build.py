@@ -53,6 +53,7 @@ def build_oracle(verbose: bool = False) -> None:
         subprocess.run(["make", "-s", "_build/liblfdoracle.so"], cwd=odir, check=True)
     if os.path.isdir("/root/reference/proj/include"):
         subprocess.run(["make", "-s", "ref"], cwd=odir, check=True)
+        subprocess.run(["make", "-s", "gpu-dropin-tests"], cwd=odir, check=True)
 
 
 def main() -> None:

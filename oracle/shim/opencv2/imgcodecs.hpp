@@ -3,6 +3,7 @@
 // reference's PNG I/O (io.hpp:116-185) is never executed; these stubs only let io.hpp parse.
 // imread returns an empty Mat and imwrite returns false, which the reference turns into IoError.
 #pragma once
+#include <algorithm>  // real OpenCV headers pull this in transitively; io.hpp relies on it
 #include <cstdint>
 #include <string>
 #include <vector>

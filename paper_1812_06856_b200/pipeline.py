@@ -38,6 +38,24 @@ def partition(n_views: int, world: int, rank: int) -> Tuple[int, int]:
     return v0, v1 - v0
 
 
+def exchange_views(t, stride: int, n_views: int, world: int, rank: int, group=None, in_place_allgather: bool = True):
+    """Make every rank's copy of an all-view buffer `t` ([n_views][stride] bytes, flat uint8)
+    complete: rank r owns views partition(n_views, world, r).  Equal blocks use one in-place
+    all-gather; otherwise each owner broadcasts its block."""
+    import torch.distributed as dist
+
+    if world == 1:
+        return
+    if in_place_allgather and n_views % world == 0:
+        chunk = stride * (n_views // world)
+        dist.all_gather_into_tensor(t, t[rank * chunk:(rank + 1) * chunk], group=group)
+        return
+    for r in range(world):
+        v0, n = partition(n_views, world, r)
+        if n:
+            dist.broadcast(t[v0 * stride:(v0 + n) * stride], src=r, group=group)
+
+
 class _CudaArray:
     """Minimal __cuda_array_interface__ over a raw device pointer (zero-copy torch view)."""
 
@@ -83,17 +101,8 @@ class HotPath:
         return torch.as_tensor(_CudaArray(ptr, nbytes), device=f"cuda:{self.ctx.device}"), stride
 
     def _allgather(self, which: int):
-        import torch.distributed as dist
-
         t, stride = self._tensor(which)
-        if self.V % self.world == 0:
-            chunk = stride * (self.V // self.world)
-            dist.all_gather_into_tensor(t, t[self.rank * chunk:(self.rank + 1) * chunk], group=self.group)
-        else:
-            for r in range(self.world):
-                v0, n = partition(self.V, self.world, r)
-                if n:
-                    dist.broadcast(t[v0 * stride:(v0 + n) * stride], src=r, group=self.group)
+        exchange_views(t, stride, self.V, self.world, self.rank, self.group)
 
     def _exchange_grids(self):
         if self.world == 1:

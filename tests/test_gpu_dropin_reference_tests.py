@@ -1,0 +1,24 @@
+"""The reference's OWN unit tests (proj/tests/test_{superpixel,sweep,refine}.cpp), compiled with
+their hot-path calls redirected to the GPU drop-in (include/lfd_gpu.hpp -> liblfdg.so, see
+oracle/gpu_dropin_test.cpp).  Every test case must pass on the B200: e.g. "plane_sweep_init
+matches the naive oracle exactly", "refinement is deterministic across worker counts",
+"uniform image yields exact square superpixels"."""
+import os
+import subprocess
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("suite", ["superpixel", "sweep", "refine"])
+def test_reference_suite_on_gpu(suite):
+    exe = os.path.join(ROOT, "oracle", "_ref", f"dropin_test_{suite}")
+    if not os.path.exists(exe):
+        pytest.skip("drop-in test binaries not built (need /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(r.stdout[-4000:], r.stderr[-2000:])
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "FAIL" not in r.stdout
