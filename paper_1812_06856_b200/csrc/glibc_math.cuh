@@ -101,6 +101,9 @@ LFDG_HD double exp_with(double x, const uint64_t* tab) {
     const double kNegLn2loN = -0x1.cf79abc9e3b3ap-47;
     const double C2 = 0x1.ffffffffffdbdp-2, C3 = 0x1.555555555543cp-3;
     const double C4 = 0x1.55555cf172b91p-5, C5 = 0x1.1111167a4d017p-7;
+    // exp(x) < 2^-1076 for x <= -746: glibc's specialcase rounds it to +0 (checked against libm
+    // over [-1100, -700], tests/test_libm_port.py).  Early out: frequent in the visibility term.
+    if (x <= -746.0) return 0.0;
     const uint64_t ux = as_u64(x);
     uint32_t abstop = (uint32_t)(ux >> 52) & 0x7ff;
     if (abstop - 0x3c9u > 0x3eu) {

@@ -54,6 +54,7 @@ struct RefineArgs {
     double max_consistency;
     int use_s, use_c, use_o;
     int kernel_px, kernel_step, radius_sp, per_dir, n_slots;
+    double uK00, uK02, uK11, uK12;  // the shared K of a kFlat view set
     unsigned long long* counters;
 };
 
@@ -120,16 +121,15 @@ __device__ __forceinline__ double smoothness_group(const RefineArgs& a, int v, i
     return acc / wsum;
 }
 
-// lround(u) for u = hx / z from q = hx * (1/z).  |q - u| <= 2^-52 |u| (two roundings), so when
-// q is farther than 8x that bound from a half-integer, u rounds to the same integer as q; the
-// nearest integer is read off the low word of q + 1.5*2^52 (round-to-nearest, no F2I).  Near a
-// half-integer (or |q| >= 2^30) it returns false and the caller divides exactly.
+// lround(u) for u = hx / z from q = hx * (1/z).  |q - u| <= 1.5 * 2^-52 |u| (two roundings), i.e.
+// <= 2^-31 for |q| < 2^20, so when q is farther than 2^-28 from a half-integer, u rounds to the
+// same integer as q; the nearest integer is read off the low word of q + 1.5*2^52
+// (round-to-nearest, no F2I).  Otherwise it returns false and the caller divides exactly.
 __device__ __forceinline__ bool fast_lround(double q, int& out) {
-    const double aq = fabs(q);
-    if (!(aq < 0x1p30)) return false;
+    if (!(fabs(q) < 0x1p20)) return false;
     const double t = q + 0x1.8p52;
     const double d = q - (t - 0x1.8p52);  // exact, in [-0.5, 0.5]
-    if (fabs(d) >= 0.5 - (aq * 0x1p-49 + 0x1p-1000)) return false;
+    if (!(fabs(d) < 0.5 - 0x1p-28)) return false;
     out = __double2loint(t);
     return true;
 }
@@ -140,8 +140,7 @@ struct TargetRow {   // one matching view of the task (refine.hpp:116-118, 46-47
     double R[9];
     double T[3];
     double K00, K01, K02, K11, K12;
-    int t;
-    int pad;
+    const float4* tcd;   // this target's gather raster
 };
 struct WarpSmem {
     double4* cand;  // [cap]   (global scratch)
@@ -172,7 +171,7 @@ __host__ __device__ inline size_t warp_smem_bytes(int N) {
 // go to a shared tile, then lane t folds target t's column in member order — the reference's
 // sequential photo_sum / vis_sum / x_count / y_nonempty of pair_stats (refine.hpp:127-163),
 // bit for bit.  Finally V + O are summed in target order (refine.hpp:193-198).
-template <bool kIdR, bool kCanonK>
+template <bool kIdR, bool kCanonK, bool kFlat>
 __device__ __forceinline__ double consistency_warp(const RefineArgs& a, const WarpSmem& w, int v, int sp, double4 p,
                                                    int m0, int n) {
     const int lane = threadIdx.x & 31;
@@ -209,10 +208,38 @@ __device__ __forceinline__ double consistency_warp(const RefineArgs& a, const Wa
                     }
                 }
             }
+            // kFlat (every R = I, every t.z = 0, one shared K): the target-frame z is s for every
+            // target, so 1/z and K02 z, K12 z are per-pixel constants.
+            double f_inv = 0, f_kz0 = 0, f_kz1 = 0;
+            if (kFlat && ok) {
+                f_inv = 1.0 / sv2;
+                f_kz0 = a.uK02 * sv2;
+                f_kz1 = a.uK12 * sv2;
+            }
             for (int tt = half; tt < nr; tt += 2) {
                 const TargetRow& g = w.tg[t0 + tt];
                 double ph = -1.0, vsv = -2.0;
-                if (ok) {
+                if (kFlat && ok) {
+                    const double hx = a.uK00 * (sv0 + g.T[0]) + f_kz0;
+                    const double hy = a.uK11 * (sv1 + g.T[1]) + f_kz1;
+                    int px, py;
+                    if (!fast_lround(hx * f_inv, px)) px = lround_int(hx / sv2);
+                    if (!fast_lround(hy * f_inv, py)) py = lround_int(hy / sv2);
+                    if ((unsigned)px < (unsigned)a.W && (unsigned)py < (unsigned)a.H) {
+                        const float4 c = __ldg(&g.tcd[py * a.W + px]);
+                        ph = libm::exp_with(-(double)color_dist2(rc.x, rc.y, rc.z, c.x, c.y, c.z) * a.inv_two_alpha2,
+                                            w.exptab);
+                        const float td = c.w;
+                        if (td > 0) {
+                            if (sv2 <= (double)td * (1.0 + 1e-6)) {
+                                const double rr = f_inv - 1.0 / (double)td;
+                                vsv = libm::exp_with(-rr * rr * a.inv_two_sigma2, w.exptab);
+                            } else {
+                                vsv = -1.0;
+                            }
+                        }
+                    }
+                } else if (!kFlat && ok) {
                     double x0, x1, x2;
                     if (kIdR) {
                         x0 = sv0 + g.T[0];
@@ -233,7 +260,7 @@ __device__ __forceinline__ double consistency_warp(const RefineArgs& a, const Wa
                         if (!(px < 0 || py < 0 || px >= a.W || py >= a.H)) {
                             // tgrid.sp[tgrid.label(px, py)].mean_color and snapshot.depth[t](px, py)
                             // (refine.hpp:146-152) in one 16-byte gather
-                            const float4 c = __ldg(&a.tcd[(size_t)g.t * hw + (size_t)py * a.W + px]);
+                            const float4 c = __ldg(&g.tcd[py * a.W + px]);
                             ph = libm::exp_with(-(double)color_dist2(rc.x, rc.y, rc.z, c.x, c.y, c.z) * a.inv_two_alpha2,
                                                 w.exptab);
                             const float td = c.w;
@@ -287,7 +314,7 @@ __device__ __forceinline__ double consistency_warp(const RefineArgs& a, const Wa
 // candidate in index order with the running prune E_s (1 + eta) <= e_cur: the same
 // candidates are evaluated as in the reference.  init: cand[0] is the current plane and its
 // energy initialises e_cur (refine.hpp:277).
-template <bool kIdR, bool kCanonK>
+template <bool kIdR, bool kCanonK, bool kFlat>
 __device__ __forceinline__ void greedy(const RefineArgs& a, const WarpSmem& w, int n, int v, int sp, int m0, int n_members,
                        bool init, double& e_cur, double4& current, unsigned& accepted,
                        unsigned long long& pix_evals, unsigned& cand_evals) {
@@ -308,7 +335,7 @@ __device__ __forceinline__ void greedy(const RefineArgs& a, const WarpSmem& w, i
         const double4 cand = w.cand[c];
         double e;
         if (a.use_c) {
-            const double ec = consistency_warp<kIdR, kCanonK>(a, w, v, sp, cand, m0, n_members);
+            const double ec = consistency_warp<kIdR, kCanonK, kFlat>(a, w, v, sp, cand, m0, n_members);
             e = prune ? w.es[c] * ec : (a.use_s ? 1.0 * w.es[c] : 1.0) * ec;
             pix_evals += (unsigned long long)a.N * n_members;
         } else {
@@ -341,7 +368,7 @@ __device__ void smoothness_all(const RefineArgs& a, const WarpSmem& w, int n, in
 
 // Persistent kernel: each warp pulls (view, superpixel) tasks from a global counter and runs
 // refine_iteration's task body (refine.hpp:269-320) for it.
-template <bool kIdR, bool kCanonK>
+template <bool kIdR, bool kCanonK, bool kFlat>
 __global__ void __launch_bounds__(128, 8) k_refine(RefineArgs a, int n_tasks, int* task_counter, int cap,
                                                 double4* g_cand, double* g_es) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -397,7 +424,7 @@ __global__ void __launch_bounds__(128, 8) k_refine(RefineArgs a, int n_tasks, in
             g.K02 = tc.K[2];
             g.K11 = tc.K[4];
             g.K12 = tc.K[5];
-            g.t = t;
+            g.tcd = a.tcd + (size_t)t * a.W * a.H;
         }
         __syncwarp();
 
@@ -405,7 +432,7 @@ __global__ void __launch_bounds__(128, 8) k_refine(RefineArgs a, int n_tasks, in
         if (lane == 0) w.cand[0] = cur0;
         __syncwarp();
         if (a.use_s) smoothness_all(a, w, 1, v, sp);
-        greedy<kIdR, kCanonK>(a, w, 1, v, sp, m0, n_members, true, e_cur, current, accepted, pix_evals, cand_evals);
+        greedy<kIdR, kCanonK, kFlat>(a, w, 1, v, sp, m0, n_members, true, e_cur, current, accepted, pix_evals, cand_evals);
 
         // ---- phase A: grid_neighbors(Kernel) order (superpixel.hpp:318-343), re-anchored
         const int gx = sp % a.gw, gy = sp / a.gw;
@@ -450,7 +477,7 @@ __global__ void __launch_bounds__(128, 8) k_refine(RefineArgs a, int n_tasks, in
         }
         __syncwarp();
         if (a.use_s) smoothness_all(a, w, n_cand, v, sp);
-        greedy<kIdR, kCanonK>(a, w, n_cand, v, sp, m0, n_members, false, e_cur, current, accepted, pix_evals, cand_evals);
+        greedy<kIdR, kCanonK, kFlat>(a, w, n_cand, v, sp, m0, n_members, false, e_cur, current, accepted, pix_evals, cand_evals);
 
         // ---- phase B: normal_candidates (refine.hpp:213-242) at the phase-A depth
         {
@@ -494,7 +521,7 @@ __global__ void __launch_bounds__(128, 8) k_refine(RefineArgs a, int n_tasks, in
             __syncwarp();
             const int nn = __popc(m);
             if (a.use_s) smoothness_all(a, w, nn, v, sp);
-            greedy<kIdR, kCanonK>(a, w, nn, v, sp, m0, n_members, false, e_cur, current, accepted, pix_evals, cand_evals);
+            greedy<kIdR, kCanonK, kFlat>(a, w, nn, v, sp, m0, n_members, false, e_cur, current, accepted, pix_evals, cand_evals);
         }
         if (lane == 0) a.out[vs + sp] = current;
         accepted_total += accepted;
@@ -693,14 +720,27 @@ void refine_iteration(Ctx& c, int l) {
             LFDG_CUDA_CHECK(cudaMemsetAsync(rd.task_counter.p, 0, sizeof(int), c.stream));
             kernel<<<blocks, 128, smem, c.stream>>>(a, n_tasks, rd.task_counter.p, cap, rd.cand.p, rd.es.p);
         };
-        if (c.identity_rot && c.canonical_k)
-            launch(k_refine<true, true>);
-        else if (c.identity_rot)
-            launch(k_refine<true, false>);
-        else if (c.canonical_k)
-            launch(k_refine<false, true>);
-        else
-            launch(k_refine<false, false>);
+        // kFlat: every rotation I, canonical and identical K, every camera centre at z = 0
+        // (then every rel_trans.z = 0): the rectified / grid rigs of the fixtures.
+        bool flat = c.identity_rot && c.canonical_k;
+        for (const lfdg_camera& k : c.cams)
+            flat = flat && k.t[2] == 0.0 && k.K[0] == c.cams[0].K[0] && k.K[2] == c.cams[0].K[2] &&
+                   k.K[4] == c.cams[0].K[4] && k.K[5] == c.cams[0].K[5];
+        if (flat) {
+            a.uK00 = c.cams[0].K[0];
+            a.uK02 = c.cams[0].K[2];
+            a.uK11 = c.cams[0].K[4];
+            a.uK12 = c.cams[0].K[5];
+            launch(k_refine<true, true, true>);
+        } else if (c.identity_rot && c.canonical_k) {
+            launch(k_refine<true, true, false>);
+        } else if (c.identity_rot) {
+            launch(k_refine<true, false, false>);
+        } else if (c.canonical_k) {
+            launch(k_refine<false, true, false>);
+        } else {
+            launch(k_refine<false, false, false>);
+        }
         LFDG_LAUNCHED(&c);
         LFDG_CUDA_CHECK(cudaMemcpyAsync(c.planes.p + (size_t)rv0 * c.nsp, c.planes_next.p + (size_t)rv0 * c.nsp,
                                         (size_t)rn * c.nsp * sizeof(double4), cudaMemcpyDeviceToDevice, c.stream));
