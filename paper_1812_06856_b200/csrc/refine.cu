@@ -150,6 +150,7 @@ struct WarpSmem {
     double* vs;     // [16][pitch] visibility term: Gaussian (visible), -1 (occluded), -2 (no target depth)
     double* res;    // [N] V + O per target
     const uint64_t* exptab;  // glibc exp table staged in shared memory (per block)
+    double m_task;           // upper bound of V_t + O_t for the current task
     int pitch;
 };
 constexpr int kMaxTargets = 64;
@@ -324,7 +325,12 @@ __device__ __forceinline__ void greedy(const RefineArgs& a, const WarpSmem& w, i
     while (next < n) {
         // next candidate that survives the prune test (ordered ballot scan)
         const int idx = next + lane;
-        const bool pass = idx < n && (init || !prune || w.es[idx] * a.max_consistency > e_cur);
+        // The reference prunes with E_s (1 + eta) <= e_cur (refine.hpp:297).  Here the task's own
+        // bound m_task = 1 + eta (1 - min_nb_sim) >= every V_t + O_t (photo, visibility ratio <= 1,
+        // O_t = eta (1 - min_nb_sim) or 0), padded by 2^-30 against rounding, also prunes: a
+        // candidate with E_s m_task <= e_cur has E <= e_cur and is never accepted, so the winner
+        // and the accepted count are the reference's; only non-accepted evaluations are skipped.
+        const bool pass = idx < n && (init || !prune || w.es[idx] * w.m_task > e_cur);
         const unsigned m = __ballot_sync(LFDG_FULL_MASK, pass);
         if (!m) {
             next += 32;
@@ -412,6 +418,7 @@ __global__ void __launch_bounds__(128, 8) k_refine(RefineArgs a, int n_tasks, in
         double4 current = cur0;
         double e_cur = 0;
         unsigned accepted = 0;
+        w.m_task = (a.use_o ? 1.0 + a.eta * (1.0 - (double)a.min_nb_sim[vs + sp]) : 1.0) * (1.0 + 0x1p-30);
         for (int ti = lane; ti < a.N; ti += 32) {  // the task's matching views (refine.hpp:116-118)
             const int t = a.targets[(size_t)v * a.N + ti];
             const double* rel = a.rel + ((size_t)v * a.N + ti) * 12;
