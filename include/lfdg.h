@@ -194,6 +194,8 @@ int lfdg_rgb_to_scaled_lab(int64_t n_pixels, const float* rgb, float* lab);
 /* Device ports of glibc exp / expf used by the energy (glibc_math.cuh), on caller inputs. */
 int lfdg_selftest_exp(int device, const double* in, double* out, size_t n);
 int lfdg_selftest_expf(int device, const float* in, float* out, size_t n);
+/* The hot-loop variant of exp for non-positive arguments (identical results). */
+int lfdg_selftest_exp_nonpos(int device, const double* in, double* out, size_t n);
 /* Measured FP64 FMA throughput of the device (FLOP/s, DFMA = 2), the sweep/refine roofline. */
 int lfdg_selftest_fp64_peak(int device, double* flops);
 

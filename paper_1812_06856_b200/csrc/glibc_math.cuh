@@ -151,6 +151,54 @@ LFDG_HD double exp_with(double x, const uint64_t* tab) {
 
 LFDG_HD double exp(double x) { return exp_with(x, nullptr); }
 
+// The same function restricted to !(x > 0) (every exp argument of the energy is minus a
+// square, refine.hpp:36/149/158): identical results (checked against libm on CPU and GPU),
+// with the branch structure reduced to the cases that can occur and the polynomial constants
+// read from constant memory, so the hot loop does not rematerialise them per call.
+#if defined(__CUDACC__)
+static __constant__ double kExpC[8] = {0x1.71547652b82fep+7, 0x1.8p+52, -0x1.62e42fefa0000p-8,
+                                       -0x1.cf79abc9e3b3ap-47, 0x1.ffffffffffdbdp-2, 0x1.555555555543cp-3,
+                                       0x1.55555cf172b91p-5, 0x1.1111167a4d017p-7};
+#endif
+static const double kExpCHost[8] = {0x1.71547652b82fep+7, 0x1.8p+52, -0x1.62e42fefa0000p-8,
+                                    -0x1.cf79abc9e3b3ap-47, 0x1.ffffffffffdbdp-2, 0x1.555555555543cp-3,
+                                    0x1.55555cf172b91p-5, 0x1.1111167a4d017p-7};
+#if defined(__CUDA_ARCH__)
+#define LFDG_EXPC(i) kExpC[i]
+#else
+#define LFDG_EXPC(i) kExpCHost[i]
+#endif
+
+LFDG_HD double exp_nonpos(double x) {
+    if (x <= -746.0) return 0.0;              // < 2^-1076: glibc rounds to +0
+    if (!(x <= -0x1p-54)) return 1.0 + x;     // |x| < 2^-54 (abstop < 0x3c9), -0.0, NaN
+    double kd = fma_(x, LFDG_EXPC(0), LFDG_EXPC(1));
+    const uint64_t ki = as_u64(kd);
+    kd = kd - LFDG_EXPC(1);
+    const double r = fma_(kd, LFDG_EXPC(3), fma_(kd, LFDG_EXPC(2), x));
+    const unsigned idx = 2u * (unsigned)(ki & 127u);
+    const double tail = as_f64(exp_tab(idx));
+    uint64_t sbits = exp_tab(idx + 1) + (ki << 45);
+    const double r2 = r * r;
+    const double tmp = fma_(r2 * r2, fma_(r, LFDG_EXPC(7), LFDG_EXPC(6)), fma_(fma_(r, LFDG_EXPC(5), LFDG_EXPC(4)), r2, r + tail));
+    if (x <= -512.0) {  // specialcase, k < 0 (abstop == 0 for 512 <= |x| < 1024)
+        sbits += 1022ull << 52;
+        const double scale = as_f64(sbits);
+        const double t = scale * tmp;
+        double y = scale + t;
+        if (y < 1.0) {
+            const double hi = y + 1.0;
+            double lo = (scale - y) + t;
+            lo = ((1.0 - hi) + y) + lo;
+            y = (lo + hi) - 1.0;
+            if (y == 0.0) y = 0.0;
+        }
+        return 0x1p-1022 * y;
+    }
+    const double scale = as_f64(sbits);
+    return fma_(scale, tmp, scale);
+}
+
 #if defined(__CUDACC__)
 // Copy the exp table into shared memory (block-cooperative); returns the smem pointer.
 __device__ __forceinline__ const uint64_t* stage_exp_table(uint64_t* smem256) {

@@ -75,7 +75,7 @@ __device__ __forceinline__ int lround_int(double x) {
 // depth_consistency (refine.hpp:34-37)
 __device__ __forceinline__ double depth_consistency(double d1, double d2, double two_sigma2) {
     const double r = 1.0 / d1 - 1.0 / d2;
-    return libm::exp(-(r * r) / two_sigma2);
+    return libm::exp_nonpos(-(r * r) / two_sigma2);
 }
 
 // ---- smoothness_term (refine.hpp:84-100), warp-parallel: lanes = (candidate, ring slot k)
@@ -228,13 +228,12 @@ __device__ __forceinline__ double consistency_warp(const RefineArgs& a, const Wa
                     if (!fast_lround(hy * f_inv, py)) py = lround_int(hy / sv2);
                     if ((unsigned)px < (unsigned)a.W && (unsigned)py < (unsigned)a.H) {
                         const float4 c = __ldg(&g.tcd[py * a.W + px]);
-                        ph = libm::exp_with(-(double)color_dist2(rc.x, rc.y, rc.z, c.x, c.y, c.z) * a.inv_two_alpha2,
-                                            w.exptab);
+                        ph = libm::exp_nonpos(-(double)color_dist2(rc.x, rc.y, rc.z, c.x, c.y, c.z) * a.inv_two_alpha2);
                         const float td = c.w;
                         if (td > 0) {
                             if (sv2 <= (double)td * (1.0 + 1e-6)) {
                                 const double rr = f_inv - 1.0 / (double)td;
-                                vsv = libm::exp_with(-rr * rr * a.inv_two_sigma2, w.exptab);
+                                vsv = libm::exp_nonpos(-rr * rr * a.inv_two_sigma2);
                             } else {
                                 vsv = -1.0;
                             }
@@ -262,13 +261,12 @@ __device__ __forceinline__ double consistency_warp(const RefineArgs& a, const Wa
                             // tgrid.sp[tgrid.label(px, py)].mean_color and snapshot.depth[t](px, py)
                             // (refine.hpp:146-152) in one 16-byte gather
                             const float4 c = __ldg(&g.tcd[py * a.W + px]);
-                            ph = libm::exp_with(-(double)color_dist2(rc.x, rc.y, rc.z, c.x, c.y, c.z) * a.inv_two_alpha2,
-                                                w.exptab);
+                            ph = libm::exp_nonpos(-(double)color_dist2(rc.x, rc.y, rc.z, c.x, c.y, c.z) * a.inv_two_alpha2);
                             const float td = c.w;
                             if (td > 0) {
                                 if (x2 <= (double)td * (1.0 + 1e-6)) {
                                     const double rr = inv_z - 1.0 / (double)td;
-                                    vsv = libm::exp_with(-rr * rr * a.inv_two_sigma2, w.exptab);
+                                    vsv = libm::exp_nonpos(-rr * rr * a.inv_two_sigma2);
                                 } else {
                                     vsv = -1.0;
                                 }

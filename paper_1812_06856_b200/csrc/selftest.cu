@@ -8,6 +8,10 @@ __global__ void k_exp(const double* in, double* out, size_t n) {
     const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) out[i] = lfdg::libm::exp(in[i]);
 }
+__global__ void k_exp_nonpos(const double* in, double* out, size_t n) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = lfdg::libm::exp_nonpos(in[i]);
+}
 __global__ void k_expf(const float* in, float* out, size_t n) {
     const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) out[i] = lfdg::libm::expf(in[i]);
@@ -34,6 +38,9 @@ int run(int device, const T* in, T* out, size_t n, K kernel) {
 
 extern "C" {
 int lfdg_selftest_exp(int device, const double* in, double* out, size_t n) { return run(device, in, out, n, k_exp); }
+int lfdg_selftest_exp_nonpos(int device, const double* in, double* out, size_t n) {
+    return run(device, in, out, n, k_exp_nonpos);
+}
 int lfdg_selftest_expf(int device, const float* in, float* out, size_t n) { return run(device, in, out, n, k_expf); }
 }
 

@@ -48,6 +48,24 @@ int main(int argc, char** argv) {
             ++bad_d;
         }
     }
+    // exp_nonpos (the hot-loop variant) on the non-positive half, incl. the special ranges
+    std::uniform_real_distribution<double> N1(-1100, 0), N2(-800, -500), N3(-1e-15, 0);
+    for (int i = 0; i < 12000000; ++i) {
+        const double x = i % 3 == 0 ? N1(rng) : i % 3 == 1 ? N2(rng) : N3(rng);
+        const double a = ::exp(x), c = lfdg::libm::exp_nonpos(x);
+        if (std::memcmp(&a, &c, 8) != 0) {
+            if (bad_d < 15) std::printf("exp_nonpos x=%a libm=%a port=%a\n", x, a, c);
+            ++bad_d;
+        }
+    }
+    for (const double x : {0.0, -0.0, -0x1p-54, -0x1.fffffffffffffp-55, -512.0, -745.13321910194110842, -746.0,
+                           -1024.0, -1e300, -(double)INFINITY, (double)NAN}) {
+        const double a = ::exp(x), c = lfdg::libm::exp_nonpos(x);
+        if (std::memcmp(&a, &c, 8) != 0 && !(std::isnan(a) && std::isnan(c))) {
+            std::printf("exp_nonpos x=%a libm=%a port=%a\n", x, a, c);
+            ++bad_d;
+        }
+    }
     std::printf("exp mismatches: %llu\n", static_cast<unsigned long long>(bad_d));
     return (bad || bad_d) ? 1 : 0;
 }

@@ -48,3 +48,17 @@ def test_expf_matches_host_libm_exhaustive_slice():
     got = out[idx]
     same = (got.view(np.uint32) == want.view(np.uint32)) | (np.isnan(got) & np.isnan(want))
     assert same.all(), f"{(~same).sum()} mismatches"
+
+
+def test_exp_nonpos_matches_host_libm():
+    from paper_1812_06856_b200 import _native as N
+
+    rng = np.random.default_rng(11)
+    x = np.concatenate([rng.uniform(-1100, 0, 300000), rng.uniform(-800, -500, 200000), rng.uniform(-1e-15, 0, 10000),
+                        np.array([0.0, -0.0, -2.0**-54, -512.0, -745.1332191019411, -746.0, -1024.0, -np.inf])])
+    x = np.ascontiguousarray(x)
+    out = np.zeros_like(x)
+    N.check(N.lib().lfdg_selftest_exp_nonpos(0, N.ptr(x), N.ptr(out), x.size))
+    L = _libm()
+    want = np.array([L.exp(float(v)) for v in x])
+    assert np.array_equal(out.view(np.uint64), want.view(np.uint64))
