@@ -1,7 +1,8 @@
 // lfd_gpu.hpp — C++ drop-in for the reference's hot path (proj/include/lfd) on B200.
 //
-// Include AFTER the reference headers (it uses their value types: ImageBuffer, SlicParams,
-// SuperpixelGrid, MultiViewSet, SweepParams, PlaneMap, RefineContext, RefineStats).  Every
+// Uses the reference's own value types (ImageBuffer, SlicParams, SuperpixelGrid, MultiViewSet,
+// SweepParams, PlaneMap, RefineContext, RefineStats, CandidateRaster), so the reference's
+// include directory (proj/include) must be on the include path.  Every
 // function has the reference's signature and semantics and marshals through the C-ABI in
 // lfdg.h (link with -llfdg):
 //
@@ -11,6 +12,9 @@
 //   lfd::gpu::rasterize         sweep.hpp:44
 //   lfd::gpu::refine_iteration  refine.hpp:253   (takes the reference's RefineContext)
 //   lfd::gpu::run_refinement    refine.hpp:325
+//   lfd::gpu::gather_candidates fusion.hpp:31
+//   lfd::gpu::stability_fuse    fusion.hpp:65
+//   lfd::gpu::fuse_all          fusion.hpp:94
 //
 // Errors are rethrown as the reference's exception classes (InvalidParams, InvariantError,
 // std::runtime_error).  `workers` is accepted and ignored: results are bit-identical to the
@@ -24,6 +28,10 @@
 #include <string>
 #include <vector>
 
+#include "lfd/fusion.hpp"
+#include "lfd/refine.hpp"
+#include "lfd/superpixel.hpp"
+#include "lfd/sweep.hpp"
 #include "lfdg.h"
 
 namespace lfd {
@@ -228,6 +236,73 @@ inline PlaneMap run_refinement(const RefineContext& ctx, PlaneMap state, int wor
         gpu::rasterize(*ctx.mvs, *ctx.grids, state);
     }
     return state;
+}
+
+// ---- fusion (fusion.hpp) --------------------------------------------------------------
+namespace detail {
+// A context over depth maps + cameras only (fusion reads no images).
+inline void set_depth_views(Context& c, const std::vector<DepthMap>& maps, const std::vector<PinholeCamera>& cameras) {
+    const int V = static_cast<int>(maps.size());
+    const int W = maps[0].width, H = maps[0].height;
+    std::vector<float> images(static_cast<std::size_t>(V) * W * H * 3, 0.f);
+    std::vector<lfdg_camera> cams(V);
+    for (int v = 0; v < V; ++v) cams[v] = Context::camera(cameras[v]);
+    check(lfdg_set_views(c.get(), V, W, H, images.data(), cams.data(), 1.0, 2.0));
+    for (int v = 0; v < V; ++v) c.set_depth(v, maps[v]);
+}
+}  // namespace detail
+
+inline CandidateRaster gather_candidates(int reference_view, const std::vector<DepthMap>& maps,
+                                          const std::vector<PinholeCamera>& cameras) {
+    detail::Context c;
+    detail::set_depth_views(c, maps, cameras);
+    const int W = maps[reference_view].width, H = maps[reference_view].height;
+    std::vector<std::int32_t> off(static_cast<std::size_t>(W) * H + 1);
+    std::int64_t total = 0;
+    detail::check(lfdg_gather_candidates(c.get(), reference_view, off.data(), nullptr, nullptr, 0, &total));
+    std::vector<float> dep(total > 0 ? total : 1);
+    std::vector<std::int32_t> vw(total > 0 ? total : 1);
+    detail::check(lfdg_gather_candidates(c.get(), reference_view, off.data(), dep.data(), vw.data(), total, &total));
+    CandidateRaster cr;
+    cr.width = W;
+    cr.height = H;
+    cr.lists.assign(static_cast<std::size_t>(W) * H, {});
+    for (std::size_t i = 0; i < cr.lists.size(); ++i)
+        for (std::int32_t k = off[i]; k < off[i + 1]; ++k) cr.lists[i].push_back({dep[k], vw[k]});
+    return cr;
+}
+
+inline DepthMap stability_fuse(const CandidateRaster& candidates, double epsilon, int workers = 1) {
+    (void)workers;
+    const int npx = static_cast<int>(candidates.lists.size());
+    std::vector<std::int32_t> off(npx + 1, 0);
+    std::vector<float> dep;
+    std::vector<std::int32_t> vw;
+    for (int i = 0; i < npx; ++i) {
+        for (const auto& c : candidates.lists[i]) {
+            dep.push_back(c.depth);
+            vw.push_back(c.source_view);
+        }
+        off[i + 1] = static_cast<std::int32_t>(dep.size());
+    }
+    DepthMap out(candidates.width, candidates.height, 0.f);
+    detail::check(lfdg_stability_fuse(0, npx, off.data(), dep.data(), vw.data(), epsilon, out.data.data()));
+    return out;
+}
+
+inline std::vector<DepthMap> fuse_all(const std::vector<DepthMap>& maps, const std::vector<PinholeCamera>& cameras,
+                                      double epsilon, int workers = 1) {
+    (void)workers;
+    detail::Context c;
+    detail::set_depth_views(c, maps, cameras);
+    detail::check(lfdg_fuse_views(c.get(), 0, static_cast<int>(maps.size()), epsilon));
+    std::vector<DepthMap> out;
+    for (std::size_t v = 0; v < maps.size(); ++v) {
+        DepthMap d(maps[v].width, maps[v].height, 0.f);
+        detail::check(lfdg_get_fused(c.get(), static_cast<int>(v), d.data.data()));
+        out.push_back(std::move(d));
+    }
+    return out;
 }
 
 }  // namespace gpu

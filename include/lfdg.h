@@ -168,6 +168,20 @@ int lfdg_refine_work(lfdg_ctx* ctx, uint64_t* pixel_evals, uint64_t* candidate_e
 /* min_neighbor_similarity table of make_refine_context (refine.hpp:71), [nsp] floats. */
 int lfdg_get_min_nb_sim(lfdg_ctx* ctx, int view, float* out);
 
+/* ---- stability fusion (fusion.hpp:31-100; SURVEY.md §8f "next" row 1) ----------------------- */
+/* fuse_all for reference views [v0, v0+n): candidates are splatted from every view's current
+ * depth raster, fused maps stay resident (lfdg_get_fused).  epsilon <= 0 -> LFDG_INVARIANT. */
+int lfdg_fuse_views(lfdg_ctx* ctx, int v0, int n, double epsilon);
+int lfdg_get_fused(lfdg_ctx* ctx, int view, float* out);
+/* gather_candidates (fusion.hpp:31): CSR lists per reference pixel in the reference's
+ * (source view, source pixel) order.  offsets [H*W+1] always filled; depths / views [total]
+ * filled when capacity >= total (call once with NULL to size). */
+int lfdg_gather_candidates(lfdg_ctx* ctx, int ref_view, int32_t* offsets, float* depths, int32_t* views,
+                           int64_t capacity, int64_t* total);
+/* stability_fuse (fusion.hpp:65) on caller lists: offsets [n_pixels+1], depths / views. */
+int lfdg_stability_fuse(int device, int n_pixels, const int32_t* offsets, const float* depths, const int32_t* views,
+                        double epsilon, float* out);
+
 /* ---- device buffers (multi-GPU all-gather plumbing) --------------------------------------- */
 /* Raw device pointer + byte size of one all-view buffer, laid out [V][per-view block]:
  * 0 labels i32[H*W], 1 centroid x f64[nsp], 2 centroid y f64[nsp], 3 mean colour f32x4[nsp],

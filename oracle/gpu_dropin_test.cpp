@@ -3,6 +3,7 @@
 // lfd::gpu::*, everything else (the tests' own brute-force oracles, energy terms, fixtures)
 // stays the reference's CPU code.  TEST INFRASTRUCTURE ONLY (oracle/Makefile gpu-dropin-tests).
 #include "lfd/fixtures.hpp"
+#include "lfd/fusion.hpp"
 #include "lfd/refine.hpp"
 #include "lfd/superpixel.hpp"
 #include "lfd/sweep.hpp"
@@ -14,5 +15,8 @@
 #define rasterize ::lfd::gpu::rasterize
 #define refine_iteration ::lfd::gpu::refine_iteration
 #define run_refinement ::lfd::gpu::run_refinement
+#define gather_candidates ::lfd::gpu::gather_candidates
+#define stability_fuse ::lfd::gpu::stability_fuse
+#define fuse_all ::lfd::gpu::fuse_all
 
 #include REF_TEST_SOURCE

@@ -80,6 +80,8 @@ def lib():
     L.ref_grid_neighbors.argtypes = [P, I, I, I, I, I, P]
     L.ref_sweep_sample.argtypes = [P, I, P, I, I, F, I, U64, I, P]
     L.ref_refine_tasks.argtypes = [P, I, P, P, I, I, P, P, P, P]
+    L.ref_fuse_all.argtypes = [P, D, I, P]
+    L.ref_gather_candidates.argtypes = [P, I, P, P, P, C.c_int64, P]
     L.ref_bad_pixel_rate.restype = D
     L.ref_bad_pixel_rate.argtypes = [I, I, I, P, P, I, P, D, D, D, I, D]
     _lib = L
@@ -162,6 +164,21 @@ class Session:
         if counts:
             return out, int(acc[0]), int(acc[1]), int(acc[2])
         return out, int(acc[0])
+
+    def fuse_all(self, epsilon, workers=1):
+        out = np.zeros((self.V, self.H, self.W), np.float32)
+        _check(self.L.ref_fuse_all(self.h, epsilon, workers, _p(out)))
+        return out
+
+    def gather_candidates(self, ref_view):
+        off = np.zeros(self.H * self.W + 1, np.int32)
+        total = np.zeros(1, np.int64)
+        _check(self.L.ref_gather_candidates(self.h, ref_view, _p(off), None, None, 0, _p(total)))
+        n = int(total[0])
+        dep = np.zeros(max(n, 1), np.float32)
+        vw = np.zeros(max(n, 1), np.int32)
+        _check(self.L.ref_gather_candidates(self.h, ref_view, _p(off), _p(dep), _p(vw), n, _p(total)))
+        return off, dep[:n], vw[:n]
 
     def matching_views(self, view, max_neighbors=0):
         out = np.zeros(self.V, np.int32)

@@ -19,6 +19,7 @@
 
 #include "lfd/eval.hpp"
 #include "lfd/fixtures.hpp"
+#include "lfd/fusion.hpp"
 #include "lfd/pipeline.hpp"
 #include "lfd/refine.hpp"
 #include "lfd/sweep.hpp"
@@ -390,6 +391,40 @@ double ref_bad_pixel_rate(int n_views, int width, int height, const float* gt_al
     }
 }
 
+
+// fuse_all (fusion.hpp:94) of the session's current depth rasters -> out [V][H*W].
+int ref_fuse_all(void* p, double epsilon, int workers, float* out) {
+    auto* s = static_cast<Session*>(p);
+    return guarded([&] {
+        const std::vector<DepthMap> fused = fuse_all(s->state.depth, s->mvs.cameras, epsilon, workers);
+        const std::size_t npx = static_cast<std::size_t>(s->mvs.width()) * s->mvs.height();
+        for (std::size_t v = 0; v < fused.size(); ++v) std::memcpy(out + v * npx, fused[v].data.data(), npx * 4);
+    });
+}
+
+// gather_candidates (fusion.hpp:31) as CSR; depths / views filled when capacity >= total.
+int ref_gather_candidates(void* p, int ref, std::int32_t* offsets, float* depths, std::int32_t* views,
+                          std::int64_t capacity, std::int64_t* total) {
+    auto* s = static_cast<Session*>(p);
+    return guarded([&] {
+        const CandidateRaster cr = gather_candidates(ref, s->state.depth, s->mvs.cameras);
+        std::int64_t k = 0;
+        for (std::size_t i = 0; i < cr.lists.size(); ++i) {
+            offsets[i] = static_cast<std::int32_t>(k);
+            k += static_cast<std::int64_t>(cr.lists[i].size());
+        }
+        offsets[cr.lists.size()] = static_cast<std::int32_t>(k);
+        *total = k;
+        if (!depths || !views || capacity < k) return;
+        k = 0;
+        for (const auto& l : cr.lists)
+            for (const auto& c : l) {
+                depths[k] = c.depth;
+                views[k] = c.source_view;
+                ++k;
+            }
+    });
+}
 
 // ---- bounded samples of the reference's per-task loop bodies (bench.py reference arm) -----
 //

@@ -18,6 +18,8 @@ from .api import (  # noqa: F401
     plane_sweep_init,
     rasterize,
     refine_iteration,
+    fuse_all,
+    stability_fuse,
     run_refinement,
     slic_segment,
     sweep_view,
@@ -26,5 +28,5 @@ from .api import (  # noqa: F401
 __all__ = [
     "DeviceContext", "EnergyParams", "MultiViewSet", "PinholeCamera", "PlaneMap", "RefineContext", "RefineStats",
     "SlicParams", "SuperpixelGrid", "SweepParams", "make_refine_context", "plane_sweep_init", "rasterize",
-    "refine_iteration", "run_refinement", "slic_segment", "sweep_view",
+    "refine_iteration", "run_refinement", "fuse_all", "stability_fuse", "slic_segment", "sweep_view",
 ]

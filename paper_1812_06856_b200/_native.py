@@ -65,6 +65,7 @@ EXPORTED = [
     "lfdg_run_refinement", "lfdg_get_min_nb_sim", "lfdg_device_buffer", "lfdg_mark_views_ready",
     "lfdg_selftest_exp", "lfdg_selftest_expf", "lfdg_render_scene", "lfdg_rgb_to_scaled_lab",
     "lfdg_upload_images", "lfdg_download_results", "lfdg_selftest_fp64_peak", "lfdg_refine_work", "lfdg_selftest_exp_nonpos",
+    "lfdg_fuse_views", "lfdg_get_fused", "lfdg_gather_candidates", "lfdg_stability_fuse",
 ]
 
 _lib = None
@@ -145,6 +146,10 @@ def lib():
         "lfdg_selftest_fp64_peak": (I, [I, C.POINTER(D)]),
         "lfdg_refine_work": (I, [P, PU64, PU64, I]),
         "lfdg_selftest_exp_nonpos": (I, [I, P, P, C.c_size_t]),
+        "lfdg_fuse_views": (I, [P, I, I, D]),
+        "lfdg_get_fused": (I, [P, I, P]),
+        "lfdg_gather_candidates": (I, [P, I, P, P, P, C.c_int64, C.POINTER(C.c_int64)]),
+        "lfdg_stability_fuse": (I, [I, I, P, P, P, D, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -296,6 +296,26 @@ class DeviceContext:
         N.check(self.L.lfdg_refine_work(self.h, C.byref(a), C.byref(b), int(reset)))
         return a.value, b.value
 
+    # -- fusion (fusion.hpp:31-100)
+    def fuse_views(self, epsilon: float, v0: int = 0, n: Optional[int] = None):
+        N.check(self.L.lfdg_fuse_views(self.h, v0, self.V - v0 if n is None else n, float(epsilon)))
+
+    def get_fused(self, view: int) -> np.ndarray:
+        out = np.zeros((self.H, self.W), np.float32)
+        N.check(self.L.lfdg_get_fused(self.h, view, N.ptr(out)))
+        return out
+
+    def gather_candidates(self, ref_view: int):
+        """CSR (offsets [H*W+1], depths, views) in the reference's (source view, pixel) order."""
+        off = np.zeros(self.H * self.W + 1, np.int32)
+        total = C.c_int64()
+        N.check(self.L.lfdg_gather_candidates(self.h, ref_view, N.ptr(off), None, None, 0, C.byref(total)))
+        dep = np.zeros(max(total.value, 1), np.float32)
+        vw = np.zeros(max(total.value, 1), np.int32)
+        N.check(self.L.lfdg_gather_candidates(self.h, ref_view, N.ptr(off), N.ptr(dep), N.ptr(vw), total.value,
+                                              C.byref(total)))
+        return off, dep[:total.value], vw[:total.value]
+
     def min_nb_sim(self, view: int) -> np.ndarray:
         gw, gh, _ = self.grid_shape(view)
         out = np.zeros(gw * gh, np.float32)
@@ -323,6 +343,27 @@ def _context_for(mvs: MultiViewSet, device: int = 0) -> DeviceContext:
 def _install_grids(ctx: DeviceContext, grids: Sequence[SuperpixelGrid]):
     for v, g in enumerate(grids):
         ctx.set_grid(v, g.cell_size, g.label_map)
+
+
+def stability_fuse(offsets: np.ndarray, depths: np.ndarray, views: np.ndarray, epsilon: float,
+                   device: int = 0) -> np.ndarray:
+    """fusion.hpp:65 — fused depth per pixel of CSR candidate lists (offsets [n+1])."""
+    offsets = np.ascontiguousarray(offsets, np.int32)
+    depths = np.ascontiguousarray(depths, np.float32)
+    views = np.ascontiguousarray(views, np.int32)
+    out = np.zeros(len(offsets) - 1, np.float32)
+    N.check(N.lib().lfdg_stability_fuse(device, len(offsets) - 1, N.ptr(offsets), N.ptr(depths), N.ptr(views),
+                                        float(epsilon), N.ptr(out)))
+    return out
+
+
+def fuse_all(mvs: MultiViewSet, depth_maps: Sequence[np.ndarray], epsilon: float) -> List[np.ndarray]:
+    """fusion.hpp:94 — stability fusion of every view's depth map (cameras from mvs)."""
+    ctx = _context_for(mvs)
+    for v, d in enumerate(depth_maps):
+        ctx.set_depth(v, d)
+    ctx.fuse_views(epsilon)
+    return [ctx.get_fused(v) for v in range(mvs.num_views())]
 
 
 def slic_segment(image: np.ndarray, params: SlicParams = SlicParams(), workers: int = 1,

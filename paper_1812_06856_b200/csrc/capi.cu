@@ -408,6 +408,41 @@ int lfdg_get_min_nb_sim(lfdg_ctx* p, int view, float* out) {
     });
 }
 
+int lfdg_fuse_views(lfdg_ctx* p, int v0, int n, double epsilon) {
+    return guarded([&] {
+        auto* c = C(p);
+        activate(c);
+        lfdg::fuse_views(*c, v0, n, epsilon);
+    });
+}
+
+int lfdg_get_fused(lfdg_ctx* p, int view, float* out) {
+    return guarded([&] {
+        auto* c = C(p);
+        activate(c);
+        c->require_view(view);
+        if (!c->fused.p) throw lfdg::Error(LFDG_STATE, "no fused maps: call lfdg_fuse_views");
+        LFDG_CUDA_CHECK(cudaMemcpyAsync(out, c->fused.p + (size_t)view * c->hw(), c->hw() * sizeof(float),
+                                        cudaMemcpyDeviceToHost, c->stream));
+        LFDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int lfdg_gather_candidates(lfdg_ctx* p, int ref_view, int32_t* offsets, float* depths, int32_t* views,
+                           int64_t capacity, int64_t* total) {
+    return guarded([&] {
+        auto* c = C(p);
+        activate(c);
+        const long long t = lfdg::gather_candidates_host(*c, ref_view, offsets, depths, views, capacity);
+        if (total) *total = t;
+    });
+}
+
+int lfdg_stability_fuse(int device, int n_pixels, const int32_t* offsets, const float* depths, const int32_t* views,
+                        double epsilon, float* out) {
+    return guarded([&] { lfdg::stability_fuse_lists(device, n_pixels, offsets, depths, views, epsilon, out); });
+}
+
 int lfdg_device_buffer(lfdg_ctx* p, int which, void** ptr, size_t* bytes, size_t* view_stride) {
     return guarded([&] {
         auto* c = C(p);

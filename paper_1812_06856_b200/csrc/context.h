@@ -108,6 +108,7 @@ struct Ctx {
     DevBuf<double4> planes, planes_next;
     DevBuf<float> depth;
     DevBuf<int> sweep_targets;  // [V][N] matching views of the last sweep
+    DevBuf<float> fused;        // [V][H*W] stability-fused depth (fusion.hpp:94)
     DevBuf<float4> tcd;  // [V][H*W] refine gather raster: (mean colour of the pixel's label, depth)
 
     // refinement
@@ -141,6 +142,11 @@ std::vector<int> matching_views(const Ctx& c, int view, int max_neighbors);    /
 void make_refine_tables(Ctx& c, const lfdg_energy_params& p, int sweep_levels);  // refine.cu
 void refine_iteration(Ctx& c, int l);                                            // refine.cu
 void upload_images(Ctx& c, int v0, int n, const float* host);                     // transfer.cu
+void fuse_views(Ctx& c, int v0, int n, double eps);                                // fusion.cu
+long long gather_candidates_host(Ctx& c, int ref, int32_t* offsets, float* depths, int32_t* views,
+                                 long long capacity);                              // fusion.cu
+void stability_fuse_lists(int device, int npx, const int32_t* offsets, const float* depths, const int32_t* views,
+                          double eps, float* out);                                 // fusion.cu
 void download_results(Ctx& c, int v0, int n, lfdg_plane* planes, float* depth);   // transfer.cu
 
 }  // namespace lfdg

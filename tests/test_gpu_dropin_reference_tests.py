@@ -1,4 +1,4 @@
-"""The reference's OWN unit tests (proj/tests/test_{superpixel,sweep,refine}.cpp), compiled with
+"""The reference's OWN unit tests (proj/tests/test_{superpixel,sweep,refine,fusion}.cpp), compiled with
 their hot-path calls redirected to the GPU drop-in (include/lfd_gpu.hpp -> liblfdg.so, see
 oracle/gpu_dropin_test.cpp).  Every test case must pass on the B200: e.g. "plane_sweep_init
 matches the naive oracle exactly", "refinement is deterministic across worker counts",
@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("suite", ["superpixel", "sweep", "refine"])
+@pytest.mark.parametrize("suite", ["superpixel", "sweep", "refine", "fusion"])
 def test_reference_suite_on_gpu(suite):
     exe = os.path.join(ROOT, "oracle", "_ref", f"dropin_test_{suite}")
     if not os.path.exists(exe):

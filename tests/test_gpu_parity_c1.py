@@ -76,3 +76,17 @@ def test_refine_bit_exact(c1):
             assert not bad.any(), f"iteration {l} view {v}: {bad.sum()} planes differ, first {np.argmax(bad)}"
             assert np.array_equal(dc.get_depth(v), rs.depth(v))
         assert (acc_g, vio_g) == (acc_r, vio_r)
+
+
+def test_bad_pixel_rate_identical(c1, ref):
+    """north_star clause: the bad-pixel rate vs synthetic ground truth (eval.hpp:45-58, nocc mask
+    :104-135, pipeline.hpp:452-466 convention) is identical — here the fused-free refined depth
+    maps are bit-identical, so the rates are equal to the last digit."""
+    sc, rs, dc = c1
+    g = ref.render_scene("cluttered", 3, 320, 240, 320.0, 0.1)
+    step = (1.0 / sc["range"][0] - 1.0 / sc["range"][1]) / 31
+    for v in range(3):
+        for region in (0, 1):
+            want = ref.bad_pixel_rate(g["gt"], sc["cams"], v, rs.depth(v), 2 * step, 0.0, 0.0, region, 2 * step)
+            got = ref.bad_pixel_rate(g["gt"], sc["cams"], v, dc.get_depth(v), 2 * step, 0.0, 0.0, region, 2 * step)
+            assert got == want and 0.0 <= got <= 100.0
