@@ -79,6 +79,32 @@ struct RefineTables {
     DevBuf<float> ring_w;           // [V][nsp][8] color_similarity to ring neighbour k (or -1: absent)
 };
 
+// Per-context scratch (device work buffers of each stage; grow-only, reused across calls).
+struct SlicScratch {
+    DevBuf<double> ccx, ccy;
+    DevBuf<float4> ccol;
+    DevBuf<int> parent, csize, orphan_idx, orphan_list, tile_cnt, tile_off;
+    DevBuf<unsigned long long> keeper;
+    DevBuf<int> adj_cnt, adj_off, adj_cur, adj, g_count, g_merged;
+    DevBuf<unsigned char> g_assigned;
+    DevBuf<int> bbox, lcnt, moff_b, queue, seen;
+};
+struct RefineScratch {
+    DevBuf<double2> mray;      // [V][H*W] member rays in CSR order
+    DevBuf<int> task_counter;  // persistent-warp work counter
+    DevBuf<double4> cand;      // per-warp candidate planes
+    DevBuf<double> es;         // per-warp smoothness bounds
+};
+struct FuseScratch {
+    DevBuf<double> xf;  // [V][12] source -> reference transforms
+    DevBuf<int> counts, offsets, cursor;
+    DevBuf<float> cdep;
+    DevBuf<long long> ckey;
+};
+struct StagingScratch {
+    DevBuf<float> buf;  // [V][H*W*3] upload staging
+};
+
 struct Ctx {
     int device = 0;
     cudaStream_t own_stream = nullptr;
@@ -115,6 +141,11 @@ struct Ctx {
     RefineTables refine;
     int refine_v0 = 0, refine_n = -1;  // -1: all views
     DevBuf<unsigned long long> counters;  // [4]: accepted, violations, pixel-evals, candidate evals
+
+    SlicScratch slic_s;
+    RefineScratch refine_s;
+    FuseScratch fuse_s;
+    StagingScratch stage_s;
 
     size_t hw() const { return static_cast<size_t>(W) * H; }
     void require_views() const {

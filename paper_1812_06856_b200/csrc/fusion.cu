@@ -145,17 +145,6 @@ __global__ void __launch_bounds__(1024) k_scan1(const int* in, int* out, int n) 
 
 inline unsigned ceil_div(size_t a, size_t b) { return (unsigned)((a + b - 1) / b); }
 
-struct FuseScratch {
-    DevBuf<FuseXf> xf;
-    DevBuf<int> counts, offsets, cursor, cview;
-    DevBuf<float> cdep;
-    DevBuf<long long> ckey;
-};
-FuseScratch& fscratch() {
-    static FuseScratch s;
-    return s;
-}
-
 // Host transforms in Eigen's order (fusion.hpp:42-43).
 std::vector<FuseXf> fuse_transforms(const Ctx& c, int ref) {
     std::vector<FuseXf> out(c.V);
@@ -175,11 +164,12 @@ std::vector<FuseXf> fuse_transforms(const Ctx& c, int ref) {
 
 // Candidate lists of reference view `ref` from every view's depth raster; returns the total.
 long long build_candidates(Ctx& c, int ref, bool ordered) {
-    FuseScratch& s = fscratch();
+    FuseScratch& s = c.fuse_s;
     const size_t hw = c.hw();
     cudaStream_t st = c.stream;
     const std::vector<FuseXf> xf = fuse_transforms(c, ref);
-    s.xf.alloc(c.V);
+    s.xf.alloc((size_t)c.V * 12);
+    static_assert(sizeof(FuseXf) == 12 * sizeof(double), "FuseXf layout");
     LFDG_CUDA_CHECK(cudaMemcpyAsync(s.xf.p, xf.data(), xf.size() * sizeof(FuseXf), cudaMemcpyHostToDevice, st));
     s.counts.alloc(hw);
     s.offsets.alloc(hw + 1);
@@ -187,7 +177,7 @@ long long build_candidates(Ctx& c, int ref, bool ordered) {
     LFDG_CUDA_CHECK(cudaMemsetAsync(s.counts.p, 0, hw * sizeof(int), st));
     LFDG_CUDA_CHECK(cudaMemsetAsync(s.cursor.p, 0, hw * sizeof(int), st));
     const dim3 g(ceil_div(hw, 256), c.V);
-    k_fuse_project<<<g, 256, 0, st>>>(c.depth.p, c.d_cams.p, s.xf.p, c.W, c.H, ref, s.counts.p, nullptr, nullptr,
+    k_fuse_project<<<g, 256, 0, st>>>(c.depth.p, c.d_cams.p, reinterpret_cast<const FuseXf*>(s.xf.p), c.W, c.H, ref, s.counts.p, nullptr, nullptr,
                                       nullptr, nullptr);
     LFDG_LAUNCHED(&c);
     k_scan1<<<1, 1024, 0, st>>>(s.counts.p, s.offsets.p, (int)hw);
@@ -197,7 +187,7 @@ long long build_candidates(Ctx& c, int ref, bool ordered) {
     LFDG_CUDA_CHECK(cudaStreamSynchronize(st));
     s.cdep.alloc(std::max(total, 1));
     s.ckey.alloc(std::max(total, 1));
-    k_fuse_project<<<g, 256, 0, st>>>(c.depth.p, c.d_cams.p, s.xf.p, c.W, c.H, ref, nullptr, s.offsets.p, s.cursor.p,
+    k_fuse_project<<<g, 256, 0, st>>>(c.depth.p, c.d_cams.p, reinterpret_cast<const FuseXf*>(s.xf.p), c.W, c.H, ref, nullptr, s.offsets.p, s.cursor.p,
                                       s.cdep.p, s.ckey.p);
     LFDG_LAUNCHED(&c);
     if (ordered) {
@@ -216,7 +206,7 @@ void fuse_views(Ctx& c, int v0, int n, double eps) {
     c.fused.alloc((size_t)c.V * c.hw());
     for (int r = v0; r < v0 + n; ++r) {
         build_candidates(c, r, false);
-        FuseScratch& s = fscratch();
+        FuseScratch& s = c.fuse_s;
         k_fuse_stability<<<ceil_div(c.hw(), 128), 128, 0, c.stream>>>((int)c.hw(), s.offsets.p, s.cdep.p, s.ckey.p,
                                                                         nullptr, eps, c.fused.p + (size_t)r * c.hw());
         LFDG_LAUNCHED(&c);
@@ -226,7 +216,7 @@ void fuse_views(Ctx& c, int v0, int n, double eps) {
 long long gather_candidates_host(Ctx& c, int ref, int32_t* offsets, float* depths, int32_t* views, long long capacity) {
     c.require_view(ref);
     const long long total = build_candidates(c, ref, true);
-    FuseScratch& s = fscratch();
+    FuseScratch& s = c.fuse_s;
     const size_t hw = c.hw();
     if (offsets)
         LFDG_CUDA_CHECK(cudaMemcpyAsync(offsets, s.offsets.p, (hw + 1) * sizeof(int), cudaMemcpyDeviceToHost, c.stream));

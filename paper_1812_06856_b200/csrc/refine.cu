@@ -20,6 +20,7 @@
 // ports (glibc_math.cuh).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "context.h"
 #include "glibc_math.cuh"
@@ -401,6 +402,7 @@ __global__ void __launch_bounds__(128, 8) k_refine(RefineArgs a, int n_tasks, in
         if (lane == 0) task = atomicAdd(task_counter, 1);
         task = __shfl_sync(LFDG_FULL_MASK, task, 0);
         if (task >= n_tasks) break;
+
         // Task order (superpixel row, view, superpixel column): warps running concurrently work on
         // the same band of image rows in every view, so the target gathers of all in-flight
         // tasks share one L2-resident band instead of streaming whole views (L2 locality).
@@ -590,17 +592,6 @@ __global__ void k_member_rays(const int32_t* __restrict__ mpix, const Cam* cams,
 
 inline unsigned ceil_div(size_t a, size_t b) { return (unsigned)((a + b - 1) / b); }
 
-struct RefineDev {
-    DevBuf<double2> mray;
-    DevBuf<int> task_counter;
-    DevBuf<double4> cand;
-    DevBuf<double> es;
-};
-RefineDev& refine_dev() {
-    static RefineDev d;
-    return d;
-}
-
 }  // namespace
 
 void make_refine_tables(Ctx& c, const lfdg_energy_params& p, int sweep_levels) {
@@ -648,7 +639,7 @@ void make_refine_tables(Ctx& c, const lfdg_energy_params& p, int sweep_levels) {
     k_color_tables<<<dim3(ceil_div(c.nsp, 128), c.V), 128, 0, st>>>(c.color.p, c.nsp, c.gw, c.gh, p.alpha,
                                                                    t.min_nb_sim.p, t.ring_w.p);
     LFDG_LAUNCHED(&c);
-    RefineDev& rd = refine_dev();
+    RefineScratch& rd = c.refine_s;
     rd.mray.alloc((size_t)c.V * c.hw());
     k_member_rays<<<dim3(ceil_div(c.hw(), 256), c.V), 256, 0, st>>>(c.mpix.p, c.d_cams.p, c.W, c.H, rd.mray.p);
     LFDG_LAUNCHED(&c);
@@ -676,7 +667,7 @@ void refine_iteration(Ctx& c, int l) {
     a.color = c.color.p;
     a.cray = c.cray.p;
     a.moff = c.moff.p;
-    a.mray = refine_dev().mray.p;
+    a.mray = c.refine_s.mray.p;
     a.planes = c.planes.p;
     a.depth = c.depth.p;
     a.tcd = c.tcd.p;
@@ -718,8 +709,7 @@ void refine_iteration(Ctx& c, int l) {
             LFDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 128, smem));
             const int n_tasks = rn * c.nsp;
             const int blocks = std::max(1, std::min(per_sm * c.sm_count, (n_tasks + 3) / 4));
-            RefineDev& rd = refine_dev();
-            rd.task_counter.alloc(1);
+            RefineScratch& rd = c.refine_s;
             rd.cand.alloc((size_t)blocks * 4 * cap);
             rd.es.alloc((size_t)blocks * 4 * cap);
             LFDG_CUDA_CHECK(cudaMemsetAsync(rd.task_counter.p, 0, sizeof(int), c.stream));

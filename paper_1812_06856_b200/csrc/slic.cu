@@ -623,26 +623,11 @@ __global__ void __launch_bounds__(32) k_empty_repair(int32_t* labels, int W, int
     }
 }
 
-struct Scratch {
-    DevBuf<double> ccx, ccy;
-    DevBuf<float4> ccol;
-    DevBuf<int> parent, csize, orphan_idx, orphan_list, tile_cnt, tile_off;
-    DevBuf<unsigned long long> keeper;
-    DevBuf<int> adj_cnt, adj_off, adj_cur, adj, g_count, g_merged;
-    DevBuf<unsigned char> g_assigned;
-    DevBuf<int> bbox, lcnt, moff_b, queue, seen;
-};
-
-Scratch& scratch() {
-    static Scratch s;  // one per process; contexts run sequentially on their stream
-    return s;
-}
-
 inline unsigned ceil_div(size_t a, size_t b) { return (unsigned)((a + b - 1) / b); }
 
 // Final stats + CSR for views [v0, v0+n) from their label maps.
 void recompute_stats(Ctx& c, int v0, int n) {
-    Scratch& s = scratch();
+    SlicScratch& s = c.slic_s;
     const size_t hw = c.hw();
     const int nsp = c.nsp;
     cudaStream_t st = c.stream;
@@ -711,7 +696,7 @@ void slic_views(Ctx& c, int v0, int n, const lfdg_slic_params& p) {
     if (c.W < p.size || c.H < p.size) throw Error(LFDG_INVALID_PARAMS, "image smaller than superpixel size");
     if (n == 0) return;
     ensure_grid_buffers(c, p.size);
-    Scratch& s = scratch();
+    SlicScratch& s = c.slic_s;
     const size_t hw = c.hw();
     const int S = p.size, gw = c.gw, gh = c.gh, nsp = c.nsp;
     const int W = c.W, H = c.H;

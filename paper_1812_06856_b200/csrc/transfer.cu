@@ -10,13 +10,6 @@ __global__ void k_repack(const float* __restrict__ src, float4* __restrict__ dst
     const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) dst[i] = make_float4(src[3 * i], src[3 * i + 1], src[3 * i + 2], 0.f);
 }
-struct Staging {
-    DevBuf<float> buf;
-};
-Staging& staging() {
-    static Staging s;
-    return s;
-}
 }  // namespace
 
 void upload_images(Ctx& c, int v0, int n, const float* host) {
@@ -24,7 +17,7 @@ void upload_images(Ctx& c, int v0, int n, const float* host) {
     if (v0 < 0 || n < 0 || v0 + n > c.V) throw Error(LFDG_STATE, "view range out of bounds");
     if (n == 0) return;
     const size_t hw = c.hw();
-    Staging& s = staging();
+    StagingScratch& s = c.stage_s;
     s.buf.alloc((size_t)c.V * hw * 3);
     LFDG_CUDA_CHECK(cudaMemcpyAsync(s.buf.p, host, (size_t)n * hw * 3 * sizeof(float), cudaMemcpyHostToDevice, c.stream));
     const size_t m = (size_t)n * hw;
