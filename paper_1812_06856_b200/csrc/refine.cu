@@ -710,6 +710,7 @@ void refine_iteration(Ctx& c, int l) {
             const int n_tasks = rn * c.nsp;
             const int blocks = std::max(1, std::min(per_sm * c.sm_count, (n_tasks + 3) / 4));
             RefineScratch& rd = c.refine_s;
+            rd.task_counter.alloc(1);
             rd.cand.alloc((size_t)blocks * 4 * cap);
             rd.es.alloc((size_t)blocks * 4 * cap);
             LFDG_CUDA_CHECK(cudaMemsetAsync(rd.task_counter.p, 0, sizeof(int), c.stream));
