@@ -56,6 +56,7 @@ struct RefineArgs {
     int use_s, use_c, use_o;
     int kernel_px, kernel_step, radius_sp, per_dir, n_slots;
     double uK00, uK02, uK11, uK12;  // the shared K of a kFlat view set
+    int row_inv;                    // kFlat and every rel_trans.y == 0: target rows are view-invariant
     unsigned long long* counters;
 };
 
@@ -213,20 +214,27 @@ __device__ __forceinline__ double consistency_warp(const RefineArgs& a, const Wa
             // kFlat (every R = I, every t.z = 0, one shared K): the target-frame z is s for every
             // target, so 1/z and K02 z, K12 z are per-pixel constants.
             double f_inv = 0, f_kz0 = 0, f_kz1 = 0;
+            int f_py = -1;
             if (kFlat && ok) {
                 f_inv = 1.0 / sv2;
                 f_kz0 = a.uK02 * sv2;
                 f_kz1 = a.uK12 * sv2;
+                if (a.row_inv) {  // every T.y = 0 (linear rig): the target row is the same for all
+                    const double hy = a.uK11 * sv1 + f_kz1;
+                    if (!fast_lround(hy * f_inv, f_py)) f_py = lround_int(hy / sv2);
+                }
             }
             for (int tt = half; tt < nr; tt += 2) {
                 const TargetRow& g = w.tg[t0 + tt];
                 double ph = -1.0, vsv = -2.0;
                 if (kFlat && ok) {
                     const double hx = a.uK00 * (sv0 + g.T[0]) + f_kz0;
-                    const double hy = a.uK11 * (sv1 + g.T[1]) + f_kz1;
-                    int px, py;
+                    int px, py = f_py;
                     if (!fast_lround(hx * f_inv, px)) px = lround_int(hx / sv2);
-                    if (!fast_lround(hy * f_inv, py)) py = lround_int(hy / sv2);
+                    if (!a.row_inv) {
+                        const double hy = a.uK11 * (sv1 + g.T[1]) + f_kz1;
+                        if (!fast_lround(hy * f_inv, py)) py = lround_int(hy / sv2);
+                    }
                     if ((unsigned)px < (unsigned)a.W && (unsigned)py < (unsigned)a.H) {
                         const float4 c = __ldg(&g.tcd[py * a.W + px]);
                         ph = libm::exp_nonpos(-(double)color_dist2(rc.x, rc.y, rc.z, c.x, c.y, c.z) * a.inv_two_alpha2);
@@ -279,21 +287,50 @@ __device__ __forceinline__ double consistency_warp(const RefineArgs& a, const Wa
                 w.vs[j * pitch + tt] = vsv;
             }
             __syncwarp();
-            if (lane < nr) {
+            {
+                // Fold in member order.  nr <= 16: the photo chain of target t runs on lane t and
+                // its visibility chain on lane 16 + t (independent sums, one code path for both);
+                // otherwise lane t runs both chains.
                 const int nb = min(kPixBlock, n - b);
-                for (int jj = 0; jj < nb; ++jj) {
-                    const double ph = w.ph[jj * pitch + lane];
-                    const double vsv = w.vs[jj * pitch + lane];
-                    if (ph >= 0) photo_sum += ph;
-                    if (vsv >= 0) {
-                        vis_sum += vsv;
-                        ++x_count;
-                    } else if (vsv == -1.0) {
-                        y_nonempty = true;
+                if (nr <= 16) {
+                    const int tl = lane & 15;
+                    const double* col = (half ? w.vs : w.ph) + tl;
+                    if (tl < nr) {
+                        for (int jj = 0; jj < nb; ++jj) {
+                            const double val = col[jj * pitch];
+                            if (val >= 0) {
+                                vis_sum += val;  // photo_sum on the photo lanes (merged below)
+                                ++x_count;
+                            } else if (val == -1.0) {
+                                y_nonempty = true;
+                            }
+                        }
+                    }
+                } else if (lane < nr) {
+                    for (int jj = 0; jj < nb; ++jj) {
+                        const double ph = w.ph[jj * pitch + lane];
+                        const double vsv = w.vs[jj * pitch + lane];
+                        if (ph >= 0) photo_sum += ph;
+                        if (vsv >= 0) {
+                            vis_sum += vsv;
+                            ++x_count;
+                        } else if (vsv == -1.0) {
+                            y_nonempty = true;
+                        }
                     }
                 }
             }
             __syncwarp();
+        }
+        if (nr <= 16) {
+            // lane t: its accumulator is photo_sum; take the visibility statistics from lane 16 + t
+            const double vs_hi = __shfl_down_sync(LFDG_FULL_MASK, vis_sum, 16);
+            const int xc_hi = __shfl_down_sync(LFDG_FULL_MASK, x_count, 16);
+            const int y_hi = __shfl_down_sync(LFDG_FULL_MASK, (int)y_nonempty, 16);
+            photo_sum = vis_sum;
+            vis_sum = vs_hi;
+            x_count = xc_hi;
+            y_nonempty = y_hi != 0;
         }
         if (lane < nr) {
             const double photo = photo_sum / (double)n;
@@ -723,6 +760,14 @@ void refine_iteration(Ctx& c, int l) {
             flat = flat && k.t[2] == 0.0 && k.K[0] == c.cams[0].K[0] && k.K[2] == c.cams[0].K[2] &&
                    k.K[4] == c.cams[0].K[4] && k.K[5] == c.cams[0].K[5];
         if (flat) {
+            a.row_inv = 1;
+            for (int vv = 0; vv < c.V; ++vv)
+                for (int i = 0; i < t.n_targets; ++i) {
+                    const lfdg_camera& cv = c.cams[vv];
+                    const lfdg_camera& ct = c.cams[t.targets_host[(size_t)vv * t.n_targets + i]];
+                    // rel_trans.y = t_t.y - (R_rel t_v).y with R_rel = I (kFlat)
+                    if (ct.t[1] - ((0.0 * cv.t[0] + 1.0 * cv.t[1]) + 0.0 * cv.t[2]) != 0.0) a.row_inv = 0;
+                }
             a.uK00 = c.cams[0].K[0];
             a.uK02 = c.cams[0].K[2];
             a.uK11 = c.cams[0].K[4];
