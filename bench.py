@@ -334,7 +334,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     roofline = {"bound": "fp64", "kernel": "k_refine (refine_iteration)", "achieved": achieved,
                 "peak": peak / 1e12, "unit": "TFLOP/s", "frac": achieved / (peak / 1e12),
                 "peak_source": "measured DFMA stream on this GPU (lfdg_selftest_fp64_peak)",
-                "traffic": None,
+                "traffic": refine_traffic(),
                 "per_launch": {"pixel_evals": pix_evals / refine_launches,
                                "flop": pix_evals * REFINE_FLOP_PER_PIXEL_EVAL / refine_launches,
                                "ms": refine_ms / refine_launches},
@@ -348,6 +348,16 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.config)
     print(json.dumps(line), flush=True)
+
+
+def refine_traffic():
+    """DRAM bytes (read + write) of one k_refine launch from the committed ncu --set full capture
+    (profiles/r1_traffic.json, see profiles/r1_ncu_k_refine.txt); None when absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+            return json.load(f)["k_refine"]["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def ctypes_fp64_peak(dev: int) -> float:
