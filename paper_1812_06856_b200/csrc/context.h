@@ -135,7 +135,7 @@ struct Ctx {
     DevBuf<float> depth;
     DevBuf<int> sweep_targets;  // [V][N] matching views of the last sweep
     DevBuf<float> fused;        // [V][H*W] stability-fused depth (fusion.hpp:94)
-    DevBuf<float4> tcd;  // [V][H*W] refine gather raster: (mean colour of the pixel's label, depth)
+    DevBuf<int4> ras;    // [V][H*W] refine gather raster: (label word, depth, 1/depth), see refine.cu
 
     // refinement
     RefineTables refine;

@@ -41,7 +41,7 @@ struct RefineArgs {
     const double2* mray;    // [V][HW] member rays in CSR order
     const double4* planes;  // snapshot [V][nsp]
     const float* depth;     // snapshot [V][HW]
-    const float4* tcd;      // [V][HW] (mean colour of the pixel's superpixel, snapshot depth)
+    const int4* ras;        // [V][HW] gather raster (label word, depth, 1/depth), k_build_raster
     double4* out;           // [V][nsp]
     // context tables
     const int* targets;     // [V][N]
@@ -137,35 +137,83 @@ __device__ __forceinline__ bool fast_lround(double q, int& out) {
 }
 
 // Per-warp shared-memory slice.  Candidate planes / upper bounds live in a per-warp global
-// scratch row (L1-resident); the per-task target table and the pixel-term tile are shared.
+// scratch row (L1-resident); the per-task target table, the photo-weight cache and the
+// pixel-term tile are shared memory.
 struct TargetRow {   // one matching view of the task (refine.hpp:116-118, 46-47)
     double R[9];
     double T[3];
     double K00, K01, K02, K11, K12;
-    const float4* tcd;   // this target's gather raster
+    const int4* ras;     // this target's gather raster (see k_build_raster)
+};
+struct TargetFlat {  // kFlat: R = I, t.z = 0 and the shared K make everything but T.x, T.y implicit
+    double T0, T1;
+    const int4* ras;
+    const void* pad;
 };
 struct WarpSmem {
     double4* cand;  // [cap]   (global scratch)
     double* es;     // [cap]   (global scratch)
-    TargetRow* tg;  // [N]
+    void* tg;       // [N] TargetRow, or TargetFlat for kFlat
+    double2* pc;    // [N][kWays] photo-weight cache: (weight, raster word of the target label)
     double* ph;     // [16][pitch] photo term of (pixel j, target tt): weight, or -1 (no sample)
     double* vs;     // [16][pitch] visibility term: Gaussian (visible), -1 (occluded), -2 (no target depth)
     double* res;    // [N] V + O per target
-    const uint64_t* exptab;  // glibc exp table staged in shared memory (per block)
-    double m_task;           // upper bound of V_t + O_t for the current task
+    double m_task;  // upper bound of V_t + O_t for the current task
     int pitch;
 };
 constexpr int kMaxTargets = 64;
 constexpr int kPixBlock = 16;  // member pixels per tile (a half-warp each; the halves split the targets)
+constexpr int kWays = 8;       // photo-cache slots per target: (gx & 3, gy & 1) of the target superpixel
 
 __host__ __device__ inline int tile_pitch(int N) {
     const int nr = N < 32 ? N : 32;
     return (nr & 1) ? nr : nr + 1;  // odd pitch: conflict-free column reads
 }
-__host__ __device__ inline size_t warp_smem_bytes(int N) {
-    const size_t b = (size_t)N * sizeof(TargetRow) + 2 * kPixBlock * (size_t)tile_pitch(N) * sizeof(double) +
-                     (size_t)N * sizeof(double);
+__host__ __device__ inline size_t target_row_bytes(bool flat) { return flat ? sizeof(TargetFlat) : sizeof(TargetRow); }
+__host__ __device__ inline size_t warp_smem_bytes(int N, bool flat) {
+    const size_t b = (size_t)N * kWays * sizeof(double2) + (size_t)N * target_row_bytes(flat) +
+                     2 * kPixBlock * (size_t)tile_pitch(N) * sizeof(double) + (size_t)N * sizeof(double);
     return (b + 127) & ~(size_t)127;
+}
+
+// Photo weight exp(-|c_ref - c_t(label)|^2 / (2 alpha^2)) of pair_stats (refine.hpp:146-150)
+// is a pure function of the task's reference colour and the target label, so the reference's
+// one-entry label cache (cached_label / cached_w) generalises to a per-task, per-warp cache:
+// kWays direct-mapped slots per target, keyed by the raster word (label | slot << 28).  A
+// lane that misses computes the weight itself (same expression, same bits) and one lane per
+// slot writes it back; hits read the identical value.  Called by every lane of the half-warp.
+// The cache-miss path, out of line so that its registers do not weigh on the hot loop; the
+// operands are re-read from memory (L1) instead of being kept live.
+__device__ __noinline__ double photo_miss(const int* target, const float4* ref, const float4* color, int nsp, int label,
+                                          double inv_two_alpha2) {
+    const float4 rc = *ref;
+    const float4 c = __ldg(&color[(size_t)(*target) * nsp + label]);
+    return libm::exp_nonpos(-(double)color_dist2(rc.x, rc.y, rc.z, c.x, c.y, c.z) * inv_two_alpha2);
+}
+
+__device__ __forceinline__ double photo_weight(const RefineArgs& a, const WarpSmem& w, int v, int sp, int tslot,
+                                               int word, bool valid) {
+    const int slot = tslot * kWays + ((unsigned)word >> 28);
+    double ph = -1.0;
+    bool hit = true;
+    if (valid) {
+        const double2 e = w.pc[slot];
+        hit = __double2loint(e.y) == word;
+        ph = e.x;
+    }
+    const unsigned am = __activemask();
+    const unsigned miss = __ballot_sync(am, !hit);
+    if (miss) {
+        if (!hit) {
+            ph = photo_miss(a.targets + (size_t)v * a.N + tslot, a.color + (size_t)v * a.nsp + sp, a.color, a.nsp,
+                            word & 0x0FFFFFFF, a.inv_two_alpha2);
+            const unsigned peers = __match_any_sync(miss, slot);
+            if ((peers & ((1u << (threadIdx.x & 31)) - 1u)) == 0)
+                w.pc[slot] = make_double2(ph, __hiloint2double(-1, word));
+        }
+        __syncwarp(am);
+    }
+    return ph;
 }
 
 // consistency_term (refine.hpp:189-199) of plane p for task (v, sp), one warp.
@@ -183,7 +231,6 @@ __device__ __forceinline__ double consistency_warp(const RefineArgs& a, const Wa
     const int N = a.N;
     if (N == 0) return 1.0;
     const size_t hw = (size_t)a.W * a.H;
-    const float4 rc = a.color[(size_t)v * a.nsp + sp];
     const double2 cr = a.cray[(size_t)v * a.nsp + sp];
     const double ax = p.x * cr.x, ay = p.x * cr.y, az = p.x;
     const double plane_num = (p.y * ax + p.z * ay) + p.w * az;
@@ -225,64 +272,69 @@ __device__ __forceinline__ double consistency_warp(const RefineArgs& a, const Wa
                 }
             }
             for (int tt = half; tt < nr; tt += 2) {
-                const TargetRow& g = w.tg[t0 + tt];
-                double ph = -1.0, vsv = -2.0;
-                if (kFlat && ok) {
-                    const double hx = a.uK00 * (sv0 + g.T[0]) + f_kz0;
-                    int px, py = f_py;
-                    if (!fast_lround(hx * f_inv, px)) px = lround_int(hx / sv2);
-                    if (!a.row_inv) {
-                        const double hy = a.uK11 * (sv1 + g.T[1]) + f_kz1;
-                        if (!fast_lround(hy * f_inv, py)) py = lround_int(hy / sv2);
-                    }
-                    if ((unsigned)px < (unsigned)a.W && (unsigned)py < (unsigned)a.H) {
-                        const float4 c = __ldg(&g.tcd[py * a.W + px]);
-                        ph = libm::exp_nonpos(-(double)color_dist2(rc.x, rc.y, rc.z, c.x, c.y, c.z) * a.inv_two_alpha2);
-                        const float td = c.w;
-                        if (td > 0) {
-                            if (sv2 <= (double)td * (1.0 + 1e-6)) {
-                                const double rr = f_inv - 1.0 / (double)td;
-                                vsv = libm::exp_nonpos(-rr * rr * a.inv_two_sigma2);
-                            } else {
-                                vsv = -1.0;
-                            }
+                // target-frame z, 1/z and the rounded pixel (refine.hpp:138-145)
+                bool in = false;
+                double zt = 0, inv_z = 0;
+                int px = 0, py = 0;
+                const int4* ras;
+                if (kFlat) {
+                    const TargetFlat& g = static_cast<const TargetFlat*>(w.tg)[t0 + tt];
+                    ras = g.ras;
+                    if (ok) {
+                        const double hx = a.uK00 * (sv0 + g.T0) + f_kz0;
+                        py = f_py;
+                        if (!fast_lround(hx * f_inv, px)) px = lround_int(hx / sv2);
+                        if (!a.row_inv) {
+                            const double hy = a.uK11 * (sv1 + g.T1) + f_kz1;
+                            if (!fast_lround(hy * f_inv, py)) py = lround_int(hy / sv2);
                         }
+                        in = (unsigned)px < (unsigned)a.W && (unsigned)py < (unsigned)a.H;
+                        zt = sv2;
+                        inv_z = f_inv;
                     }
-                } else if (!kFlat && ok) {
-                    double x0, x1, x2;
-                    if (kIdR) {
-                        x0 = sv0 + g.T[0];
-                        x1 = sv1 + g.T[1];
-                        x2 = sv2 + g.T[2];
-                    } else {
-                        x0 = ((g.R[0] * sv0 + g.R[1] * sv1) + g.R[2] * sv2) + g.T[0];
-                        x1 = ((g.R[3] * sv0 + g.R[4] * sv1) + g.R[5] * sv2) + g.T[1];
-                        x2 = ((g.R[6] * sv0 + g.R[7] * sv1) + g.R[8] * sv2) + g.T[2];
-                    }
-                    if (x2 > 0) {
-                        const double hx = kCanonK ? g.K00 * x0 + g.K02 * x2 : (g.K00 * x0 + g.K01 * x1) + g.K02 * x2;
-                        const double hy = g.K11 * x1 + g.K12 * x2;
-                        const double inv_z = 1.0 / x2;
-                        int px, py;
-                        if (!fast_lround(hx * inv_z, px)) px = lround_int(hx / x2);
-                        if (!fast_lround(hy * inv_z, py)) py = lround_int(hy / x2);
-                        if (!(px < 0 || py < 0 || px >= a.W || py >= a.H)) {
-                            // tgrid.sp[tgrid.label(px, py)].mean_color and snapshot.depth[t](px, py)
-                            // (refine.hpp:146-152) in one 16-byte gather
-                            const float4 c = __ldg(&g.tcd[py * a.W + px]);
-                            ph = libm::exp_nonpos(-(double)color_dist2(rc.x, rc.y, rc.z, c.x, c.y, c.z) * a.inv_two_alpha2);
-                            const float td = c.w;
-                            if (td > 0) {
-                                if (x2 <= (double)td * (1.0 + 1e-6)) {
-                                    const double rr = inv_z - 1.0 / (double)td;
-                                    vsv = libm::exp_nonpos(-rr * rr * a.inv_two_sigma2);
-                                } else {
-                                    vsv = -1.0;
-                                }
-                            }
+                } else {
+                    const TargetRow& g = static_cast<const TargetRow*>(w.tg)[t0 + tt];
+                    ras = g.ras;
+                    if (ok) {
+                        double x0, x1, x2;
+                        if (kIdR) {
+                            x0 = sv0 + g.T[0];
+                            x1 = sv1 + g.T[1];
+                            x2 = sv2 + g.T[2];
+                        } else {
+                            x0 = ((g.R[0] * sv0 + g.R[1] * sv1) + g.R[2] * sv2) + g.T[0];
+                            x1 = ((g.R[3] * sv0 + g.R[4] * sv1) + g.R[5] * sv2) + g.T[1];
+                            x2 = ((g.R[6] * sv0 + g.R[7] * sv1) + g.R[8] * sv2) + g.T[2];
+                        }
+                        if (x2 > 0) {
+                            const double hx = kCanonK ? g.K00 * x0 + g.K02 * x2 : (g.K00 * x0 + g.K01 * x1) + g.K02 * x2;
+                            const double hy = g.K11 * x1 + g.K12 * x2;
+                            inv_z = 1.0 / x2;
+                            if (!fast_lround(hx * inv_z, px)) px = lround_int(hx / x2);
+                            if (!fast_lround(hy * inv_z, py)) py = lround_int(hy / x2);
+                            in = !(px < 0 || py < 0 || px >= a.W || py >= a.H);
+                            zt = x2;
                         }
                     }
                 }
+                // tgrid.label(px, py) and snapshot.depth[t](px, py) (refine.hpp:146-152) in one
+                // 16-byte gather: (label word, depth, 1 / (double)depth)
+                int word = 0;
+                double vsv = -2.0;
+                if (in) {
+                    const int4 r = __ldg(&ras[py * a.W + px]);
+                    word = r.x;
+                    const float td = __int_as_float(r.y);
+                    if (!(td <= 0)) {
+                        if (zt <= (double)td * (1.0 + 1e-6)) {
+                            const double rr = inv_z - __hiloint2double(r.w, r.z);
+                            vsv = libm::exp_nonpos(-rr * rr * a.inv_two_sigma2);
+                        } else {
+                            vsv = -1.0;
+                        }
+                    }
+                }
+                const double ph = photo_weight(a, w, v, sp, t0 + tt, word, in);
                 w.ph[j * pitch + tt] = ph;
                 w.vs[j * pitch + tt] = vsv;
             }
@@ -294,10 +346,10 @@ __device__ __forceinline__ double consistency_warp(const RefineArgs& a, const Wa
                 const int nb = min(kPixBlock, n - b);
                 if (nr <= 16) {
                     const int tl = lane & 15;
-                    const double* col = (half ? w.vs : w.ph) + tl;
+                    const double* colp = (half ? w.vs : w.ph) + tl;
                     if (tl < nr) {
                         for (int jj = 0; jj < nb; ++jj) {
-                            const double val = col[jj * pitch];
+                            const double val = colp[jj * pitch];
                             if (val >= 0) {
                                 vis_sum += val;  // photo_sum on the photo lanes (merged below)
                                 ++x_count;
@@ -414,20 +466,17 @@ template <bool kIdR, bool kCanonK, bool kFlat>
 __global__ void __launch_bounds__(128, 8) k_refine(RefineArgs a, int n_tasks, int* task_counter, int cap,
                                                 double4* g_cand, double* g_es) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ uint64_t s_exptab[256];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int gwarp = blockIdx.x * 4 + warp;
-    libm::stage_exp_table(s_exptab);
-    __syncthreads();
-    unsigned char* base = smem_raw + warp * warp_smem_bytes(a.N);
+    unsigned char* base = smem_raw + warp * warp_smem_bytes(a.N, kFlat);
     WarpSmem w;
     w.pitch = tile_pitch(a.N);
-    w.tg = reinterpret_cast<TargetRow*>(base);
-    w.ph = reinterpret_cast<double*>(base + (size_t)a.N * sizeof(TargetRow));
+    w.pc = reinterpret_cast<double2*>(base);
+    w.tg = base + (size_t)a.N * kWays * sizeof(double2);
+    w.ph = reinterpret_cast<double*>(base + (size_t)a.N * kWays * sizeof(double2) + (size_t)a.N * target_row_bytes(kFlat));
     w.vs = w.ph + kPixBlock * w.pitch;
     w.res = w.vs + kPixBlock * w.pitch;
-    w.exptab = s_exptab;
     w.cand = g_cand + (size_t)gwarp * cap;
     w.es = g_es + (size_t)gwarp * cap;
 
@@ -459,17 +508,26 @@ __global__ void __launch_bounds__(128, 8) k_refine(RefineArgs a, int n_tasks, in
         for (int ti = lane; ti < a.N; ti += 32) {  // the task's matching views (refine.hpp:116-118)
             const int t = a.targets[(size_t)v * a.N + ti];
             const double* rel = a.rel + ((size_t)v * a.N + ti) * 12;
-            TargetRow& g = w.tg[ti];
-            for (int k = 0; k < 9; ++k) g.R[k] = rel[k];
-            for (int k = 0; k < 3; ++k) g.T[k] = rel[9 + k];
-            const Cam& tc = a.cams[t];
-            g.K00 = tc.K[0];
-            g.K01 = tc.K[1];
-            g.K02 = tc.K[2];
-            g.K11 = tc.K[4];
-            g.K12 = tc.K[5];
-            g.tcd = a.tcd + (size_t)t * a.W * a.H;
+            if (kFlat) {
+                TargetFlat& g = static_cast<TargetFlat*>(w.tg)[ti];
+                g.T0 = rel[9];
+                g.T1 = rel[10];
+                g.ras = a.ras + (size_t)t * a.W * a.H;
+            } else {
+                TargetRow& g = static_cast<TargetRow*>(w.tg)[ti];
+                for (int k = 0; k < 9; ++k) g.R[k] = rel[k];
+                for (int k = 0; k < 3; ++k) g.T[k] = rel[9 + k];
+                const Cam& tc = a.cams[t];
+                g.K00 = tc.K[0];
+                g.K01 = tc.K[1];
+                g.K02 = tc.K[2];
+                g.K11 = tc.K[4];
+                g.K12 = tc.K[5];
+                g.ras = a.ras + (size_t)t * a.W * a.H;
+            }
         }
+        for (int k = lane; k < a.N * kWays; k += 32)  // new reference colour: empty photo cache
+            w.pc[k] = make_double2(0.0, __hiloint2double(-1, -1));
         __syncwarp();
 
         // ---- e_cur = energy(current) (refine.hpp:277)
@@ -602,17 +660,23 @@ __global__ void k_color_tables(const float4* __restrict__ color, int nsp, int gw
     min_nb_sim[(size_t)v * nsp + sp] = m;
 }
 
-// Refine gather raster for every view: tcd[v][p] = (mean colour of label(p), depth(p)), the
-// target-side operands of pair_stats (refine.hpp:146-152) in one 16-byte record per pixel.
-__global__ void k_build_tcd(const int32_t* __restrict__ labels, const float4* __restrict__ color,
-                            const float* __restrict__ depth, int W, int H, int nsp, float4* tcd) {
+// Refine gather raster for every view, rebuilt from the snapshot each iteration: the target-side
+// operands of pair_stats (refine.hpp:146-155) in one 16-byte record per pixel —
+//   .x  label | ((gx & 3) | (gy & 1) << 2) << 28   (photo-cache key and slot of the label)
+//   .y  snapshot depth (float bits)
+//   .zw 1.0 / (double)depth, the operand of depth_consistency's 1/td (refine.hpp:158)
+__global__ void k_build_raster(const int32_t* __restrict__ labels, const float* __restrict__ depth, int W, int H,
+                               int gw, int4* ras) {
     const size_t hw = (size_t)W * H;
     const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= hw) return;
     const int v = blockIdx.y;
-    const float4 c = color[(size_t)v * nsp + labels[(size_t)v * hw + i]];
+    const int lab = labels[(size_t)v * hw + i];
     const float td = depth[(size_t)v * hw + i];
-    tcd[(size_t)v * hw + i] = make_float4(c.x, c.y, c.z, td);
+    const int gx = lab % gw, gy = lab / gw;
+    const int word = lab | (((gx & 3) | ((gy & 1) << 2)) << 28);
+    const double inv = 1.0 / (double)td;
+    ras[(size_t)v * hw + i] = make_int4(word, __float_as_int(td), __double2loint(inv), __double2hiint(inv));
 }
 
 // Member rays in CSR order: mray[v][k] = ray(pixel mpix[v][k]) (geometry.hpp:45).
@@ -680,7 +744,8 @@ void make_refine_tables(Ctx& c, const lfdg_energy_params& p, int sweep_levels) {
     rd.mray.alloc((size_t)c.V * c.hw());
     k_member_rays<<<dim3(ceil_div(c.hw(), 256), c.V), 256, 0, st>>>(c.mpix.p, c.d_cams.p, c.W, c.H, rd.mray.p);
     LFDG_LAUNCHED(&c);
-    c.tcd.alloc((size_t)c.V * c.hw());
+    if ((size_t)c.nsp >= (1u << 28)) throw Error(LFDG_INVALID_PARAMS, "too many superpixels per view");
+    c.ras.alloc((size_t)c.V * c.hw());
     t.ready = true;
 }
 
@@ -707,7 +772,7 @@ void refine_iteration(Ctx& c, int l) {
     a.mray = c.refine_s.mray.p;
     a.planes = c.planes.p;
     a.depth = c.depth.p;
-    a.tcd = c.tcd.p;
+    a.ras = c.ras.p;
     a.out = c.planes_next.p;
     a.targets = t.targets.p;
     a.rel = t.rel.p;
@@ -734,11 +799,15 @@ void refine_iteration(Ctx& c, int l) {
     a.counters = c.counters.p;
     if (a.N > kMaxTargets) throw Error(LFDG_INVALID_PARAMS, "too many matching views (max 64)");
     const int cap = std::max(a.n_slots, 8) + 1;
-    const size_t smem = 4 * warp_smem_bytes(a.N);
+    bool flat = c.identity_rot && c.canonical_k;
+    for (const lfdg_camera& k : c.cams)
+        flat = flat && k.t[2] == 0.0 && k.K[0] == c.cams[0].K[0] && k.K[2] == c.cams[0].K[2] &&
+               k.K[4] == c.cams[0].K[4] && k.K[5] == c.cams[0].K[5];
+    const size_t smem = 4 * warp_smem_bytes(a.N, flat);
     if (rn > 0) {
-        // the refine gather raster from the current snapshot (labels, colours, depth)
-        k_build_tcd<<<dim3(ceil_div(c.hw(), 256), c.V), 256, 0, c.stream>>>(c.labels.p, c.color.p, c.depth.p, c.W,
-                                                                             c.H, c.nsp, c.tcd.p);
+        // the refine gather raster from the current snapshot (labels, depth)
+        k_build_raster<<<dim3(ceil_div(c.hw(), 256), c.V), 256, 0, c.stream>>>(c.labels.p, c.depth.p, c.W, c.H, c.gw,
+                                                                                c.ras.p);
         LFDG_LAUNCHED(&c);
         auto launch = [&](auto kernel) {
             LFDG_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -753,12 +822,8 @@ void refine_iteration(Ctx& c, int l) {
             LFDG_CUDA_CHECK(cudaMemsetAsync(rd.task_counter.p, 0, sizeof(int), c.stream));
             kernel<<<blocks, 128, smem, c.stream>>>(a, n_tasks, rd.task_counter.p, cap, rd.cand.p, rd.es.p);
         };
-        // kFlat: every rotation I, canonical and identical K, every camera centre at z = 0
-        // (then every rel_trans.z = 0): the rectified / grid rigs of the fixtures.
-        bool flat = c.identity_rot && c.canonical_k;
-        for (const lfdg_camera& k : c.cams)
-            flat = flat && k.t[2] == 0.0 && k.K[0] == c.cams[0].K[0] && k.K[2] == c.cams[0].K[2] &&
-                   k.K[4] == c.cams[0].K[4] && k.K[5] == c.cams[0].K[5];
+        // kFlat (flat above): every rotation I, canonical and identical K, every camera centre at
+        // z = 0 (then every rel_trans.z = 0): the rectified / grid rigs of the fixtures.
         if (flat) {
             a.row_inv = 1;
             for (int vv = 0; vv < c.V; ++vv)
