@@ -155,8 +155,9 @@ struct WarpSmem {
     double* es;     // [cap]   (global scratch)
     void* tg;       // [N] TargetRow, or TargetFlat for kFlat
     double2* pc;    // [N][kWays] photo-weight cache: (weight, raster word of the target label)
-    double* ph;     // [16][pitch] photo term of (pixel j, target tt): weight, or -1 (no sample)
-    double* vs;     // [16][pitch] visibility term: Gaussian (visible), -1 (occluded), -2 (no target depth)
+    double2* tile;  // [16][pitch] per (pixel j, target tt): (photo term: weight, or -1 = no sample;
+                    // visibility term: Gaussian (visible), -1 (occluded), -2 (no target depth));
+                    // kFlat first stages the pixel's raster record (label word, depth, 1/depth) there
     double* res;    // [N] V + O per target
     double m_task;  // upper bound of V_t + O_t for the current task
     int pitch;
@@ -181,7 +182,7 @@ __host__ __device__ inline size_t warp_smem_bytes(int N, bool flat) {
 // one-entry label cache (cached_label / cached_w) generalises to a per-task, per-warp cache:
 // kWays direct-mapped slots per target, keyed by the raster word (label | slot << 28).  A
 // lane that misses computes the weight itself (same expression, same bits) and one lane per
-// slot writes it back; hits read the identical value.  Called by every lane of the half-warp.
+// slot writes it back; hits read the identical value.  am: the converged lanes calling it.
 // The cache-miss path, out of line so that its registers do not weigh on the hot loop; the
 // operands are re-read from memory (L1) instead of being kept live.
 __device__ __noinline__ double photo_miss(const int* target, const float4* ref, const float4* color, int nsp, int label,
@@ -192,7 +193,7 @@ __device__ __noinline__ double photo_miss(const int* target, const float4* ref, 
 }
 
 __device__ __forceinline__ double photo_weight(const RefineArgs& a, const WarpSmem& w, int v, int sp, int tslot,
-                                               int word, bool valid) {
+                                               int word, bool valid, unsigned am) {
     const int slot = tslot * kWays + ((unsigned)word >> 28);
     double ph = -1.0;
     bool hit = true;
@@ -201,7 +202,6 @@ __device__ __forceinline__ double photo_weight(const RefineArgs& a, const WarpSm
         hit = __double2loint(e.y) == word;
         ph = e.x;
     }
-    const unsigned am = __activemask();
     const unsigned miss = __ballot_sync(am, !hit);
     if (miss) {
         if (!hit) {
@@ -239,8 +239,8 @@ __device__ __forceinline__ double consistency_warp(const RefineArgs& a, const Wa
     for (int t0 = 0; t0 < N; t0 += 32) {
         const int nr = min(32, N - t0);
         double photo_sum = 0, vis_sum = 0;
-        int x_count = 0;
-        bool y_nonempty = false;
+        int neg = 0;             // fold lanes: tile entries that are not addends (-0.0)
+        unsigned occbits = 0;    // compute lanes: bit k = some pixel of target half + 2k occluded
         for (int b = 0; b < n; b += kPixBlock) {
             const int i = b + j;
             bool ok = false;
@@ -271,50 +271,82 @@ __device__ __forceinline__ double consistency_warp(const RefineArgs& a, const Wa
                     if (!fast_lround(hy * f_inv, f_py)) f_py = lround_int(hy / sv2);
                 }
             }
-            for (int tt = half; tt < nr; tt += 2) {
-                // target-frame z, 1/z and the rounded pixel (refine.hpp:138-145)
-                bool in = false;
-                double zt = 0, inv_z = 0;
-                int px = 0, py = 0;
-                const int4* ras;
-                if (kFlat) {
+            if (kFlat) {
+                // Two phases so that the raster gathers of all of this lane's targets are in flight
+                // together: (1) project and start a 16-byte cp.async of each target's record into
+                // the tile (or mark it out of bounds), (2) wait, then turn each record into the
+                // (photo, visibility) pair in place.
+                for (int tt = half; tt < nr; tt += 2) {
                     const TargetFlat& g = static_cast<const TargetFlat*>(w.tg)[t0 + tt];
-                    ras = g.ras;
+                    double2* e = &w.tile[j * pitch + tt];
+                    bool in = false;
+                    int px = 0, py = f_py;
                     if (ok) {
                         const double hx = a.uK00 * (sv0 + g.T0) + f_kz0;
-                        py = f_py;
                         if (!fast_lround(hx * f_inv, px)) px = lround_int(hx / sv2);
                         if (!a.row_inv) {
                             const double hy = a.uK11 * (sv1 + g.T1) + f_kz1;
                             if (!fast_lround(hy * f_inv, py)) py = lround_int(hy / sv2);
                         }
                         in = (unsigned)px < (unsigned)a.W && (unsigned)py < (unsigned)a.H;
-                        zt = sv2;
-                        inv_z = f_inv;
                     }
-                } else {
-                    const TargetRow& g = static_cast<const TargetRow*>(w.tg)[t0 + tt];
-                    ras = g.ras;
-                    if (ok) {
-                        double x0, x1, x2;
-                        if (kIdR) {
-                            x0 = sv0 + g.T[0];
-                            x1 = sv1 + g.T[1];
-                            x2 = sv2 + g.T[2];
-                        } else {
-                            x0 = ((g.R[0] * sv0 + g.R[1] * sv1) + g.R[2] * sv2) + g.T[0];
-                            x1 = ((g.R[3] * sv0 + g.R[4] * sv1) + g.R[5] * sv2) + g.T[1];
-                            x2 = ((g.R[6] * sv0 + g.R[7] * sv1) + g.R[8] * sv2) + g.T[2];
+                    if (in) {
+                        const unsigned dst = (unsigned)__cvta_generic_to_shared(e);
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(g.ras + py * a.W + px)
+                                     : "memory");
+                    } else {
+                        *reinterpret_cast<int*>(e) = -1;
+                    }
+                }
+                asm volatile("cp.async.wait_all;\n" ::: "memory");
+                for (int tt = half; tt < nr; tt += 2) {
+                    double2* e = &w.tile[j * pitch + tt];
+                    const int4 r = *reinterpret_cast<const int4*>(e);
+                    const bool in = r.x >= 0;
+                    double vsv = -2.0;
+                    if (in) {
+                        const float td = __int_as_float(r.y);
+                        if (!(td <= 0)) {
+                            if (sv2 <= (double)td * (1.0 + 1e-6)) {
+                                const double rr = f_inv - __hiloint2double(r.w, r.z);
+                                vsv = libm::exp_nonpos(-rr * rr * a.inv_two_sigma2);
+                            } else {
+                                vsv = -1.0;
+                            }
                         }
-                        if (x2 > 0) {
-                            const double hx = kCanonK ? g.K00 * x0 + g.K02 * x2 : (g.K00 * x0 + g.K01 * x1) + g.K02 * x2;
-                            const double hy = g.K11 * x1 + g.K12 * x2;
-                            inv_z = 1.0 / x2;
-                            if (!fast_lround(hx * inv_z, px)) px = lround_int(hx / x2);
-                            if (!fast_lround(hy * inv_z, py)) py = lround_int(hy / x2);
-                            in = !(px < 0 || py < 0 || px >= a.W || py >= a.H);
-                            zt = x2;
-                        }
+                    }
+                    const unsigned am = __activemask();  // both halves, or the even half alone (odd nr)
+                    const double ph = photo_weight(a, w, v, sp, t0 + tt, r.x, in, am);
+                    occbits |= (vsv == -1.0 ? 1u : 0u) << (tt >> 1);
+                    *e = make_double2(in ? ph : -0.0, vsv >= 0 ? vsv : -0.0);
+                }
+            } else {
+            for (int tt = half; tt < nr; tt += 2) {
+                // target-frame z, 1/z and the rounded pixel (refine.hpp:138-145)
+                bool in = false;
+                double zt = 0, inv_z = 0;
+                int px = 0, py = 0;
+                const TargetRow& g = static_cast<const TargetRow*>(w.tg)[t0 + tt];
+                const int4* ras = g.ras;
+                if (ok) {
+                    double x0, x1, x2;
+                    if (kIdR) {
+                        x0 = sv0 + g.T[0];
+                        x1 = sv1 + g.T[1];
+                        x2 = sv2 + g.T[2];
+                    } else {
+                        x0 = ((g.R[0] * sv0 + g.R[1] * sv1) + g.R[2] * sv2) + g.T[0];
+                        x1 = ((g.R[3] * sv0 + g.R[4] * sv1) + g.R[5] * sv2) + g.T[1];
+                        x2 = ((g.R[6] * sv0 + g.R[7] * sv1) + g.R[8] * sv2) + g.T[2];
+                    }
+                    if (x2 > 0) {
+                        const double hx = kCanonK ? g.K00 * x0 + g.K02 * x2 : (g.K00 * x0 + g.K01 * x1) + g.K02 * x2;
+                        const double hy = g.K11 * x1 + g.K12 * x2;
+                        inv_z = 1.0 / x2;
+                        if (!fast_lround(hx * inv_z, px)) px = lround_int(hx / x2);
+                        if (!fast_lround(hy * inv_z, py)) py = lround_int(hy / x2);
+                        in = !(px < 0 || py < 0 || px >= a.W || py >= a.H);
+                        zt = x2;
                     }
                 }
                 // tgrid.label(px, py) and snapshot.depth[t](px, py) (refine.hpp:146-152) in one
@@ -334,56 +366,55 @@ __device__ __forceinline__ double consistency_warp(const RefineArgs& a, const Wa
                         }
                     }
                 }
-                const double ph = photo_weight(a, w, v, sp, t0 + tt, word, in);
-                w.ph[j * pitch + tt] = ph;
-                w.vs[j * pitch + tt] = vsv;
+                const unsigned am = __activemask();  // both halves, or the even half alone (odd nr)
+                const double ph = photo_weight(a, w, v, sp, t0 + tt, word, in, am);
+                occbits |= (vsv == -1.0 ? 1u : 0u) << (tt >> 1);
+                w.tile[j * pitch + tt] = make_double2(in ? ph : -0.0, vsv >= 0 ? vsv : -0.0);
+            }
             }
             __syncwarp();
-            {
-                // Fold in member order.  nr <= 16: the photo chain of target t runs on lane t and
-                // its visibility chain on lane 16 + t (independent sums, one code path for both);
-                // otherwise lane t runs both chains.
-                const int nb = min(kPixBlock, n - b);
-                if (nr <= 16) {
-                    const int tl = lane & 15;
-                    const double* colp = (half ? w.vs : w.ph) + tl;
-                    if (tl < nr) {
-                        for (int jj = 0; jj < nb; ++jj) {
-                            const double val = colp[jj * pitch];
-                            if (val >= 0) {
-                                vis_sum += val;  // photo_sum on the photo lanes (merged below)
-                                ++x_count;
-                            } else if (val == -1.0) {
-                                y_nonempty = true;
-                            }
-                        }
+            // Fold in member order: pair_stats' sequential photo_sum / vis_sum (refine.hpp:
+            // 147-158).  The tile holds addends only — a pixel that adds nothing holds -0.0, an
+            // exact identity of these sums (non-negative terms from +0.0) — so the fold is a
+            // plain chain; the sign bit counts the non-visible entries (x_count) on the way.
+            // nr <= 16: the photo chain of target t runs on lane t and its visibility chain on
+            // lane 16 + t; otherwise lane t runs both.  Rows past the last member hold -0.0.
+            if (nr <= 16) {
+                const int tl = lane & 15;
+                const double* colp = reinterpret_cast<const double*>(w.tile + tl) + half;
+                if (tl < nr) {
+#pragma unroll
+                    for (int jj = 0; jj < kPixBlock; ++jj) {
+                        const double val = colp[2 * jj * pitch];
+                        vis_sum += val;  // photo_sum on the photo lanes (merged below)
+                        neg += (unsigned)__double2hiint(val) >> 31;
                     }
-                } else if (lane < nr) {
-                    for (int jj = 0; jj < nb; ++jj) {
-                        const double ph = w.ph[jj * pitch + lane];
-                        const double vsv = w.vs[jj * pitch + lane];
-                        if (ph >= 0) photo_sum += ph;
-                        if (vsv >= 0) {
-                            vis_sum += vsv;
-                            ++x_count;
-                        } else if (vsv == -1.0) {
-                            y_nonempty = true;
-                        }
-                    }
+                }
+            } else if (lane < nr) {
+#pragma unroll 4
+                for (int jj = 0; jj < kPixBlock; ++jj) {
+                    const double2 e = w.tile[jj * pitch + lane];
+                    photo_sum += e.x;
+                    vis_sum += e.y;
+                    neg += (unsigned)__double2hiint(e.y) >> 31;
                 }
             }
             __syncwarp();
         }
         if (nr <= 16) {
             // lane t: its accumulator is photo_sum; take the visibility statistics from lane 16 + t
-            const double vs_hi = __shfl_down_sync(LFDG_FULL_MASK, vis_sum, 16);
-            const int xc_hi = __shfl_down_sync(LFDG_FULL_MASK, x_count, 16);
-            const int y_hi = __shfl_down_sync(LFDG_FULL_MASK, (int)y_nonempty, 16);
             photo_sum = vis_sum;
-            vis_sum = vs_hi;
-            x_count = xc_hi;
-            y_nonempty = y_hi != 0;
+            vis_sum = __shfl_down_sync(LFDG_FULL_MASK, vis_sum, 16);
+            neg = __shfl_down_sync(LFDG_FULL_MASK, neg, 16);
         }
+        const int x_count = kPixBlock * ((n + kPixBlock - 1) / kPixBlock) - neg;
+        // y_nonempty of target t: any occluded pixel among the 16 compute lanes of half t & 1
+        unsigned ym = 0;
+        for (int k = 0; k < (nr + 1) / 2; ++k) {
+            const unsigned m = __ballot_sync(LFDG_FULL_MASK, (occbits >> k) & 1u);
+            if ((lane >> 1) == k) ym = m;
+        }
+        const bool y_nonempty = ((lane & 1) ? (ym >> 16) : (ym & 0xFFFFu)) != 0;
         if (lane < nr) {
             const double photo = photo_sum / (double)n;
             const double vis = x_count > 0 ? photo * (vis_sum / x_count) : 0.0;
@@ -463,7 +494,10 @@ __device__ void smoothness_all(const RefineArgs& a, const WarpSmem& w, int n, in
 // Persistent kernel: each warp pulls (view, superpixel) tasks from a global counter and runs
 // refine_iteration's task body (refine.hpp:269-320) for it.
 template <bool kIdR, bool kCanonK, bool kFlat>
-__global__ void __launch_bounds__(128, 8) k_refine(RefineArgs a, int n_tasks, int* task_counter, int cap,
+#ifndef LFDG_REFINE_MIN_BLOCKS
+#define LFDG_REFINE_MIN_BLOCKS 8
+#endif
+__global__ void __launch_bounds__(128, LFDG_REFINE_MIN_BLOCKS) k_refine(RefineArgs a, int n_tasks, int* task_counter, int cap,
                                                 double4* g_cand, double* g_es) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
@@ -474,9 +508,8 @@ __global__ void __launch_bounds__(128, 8) k_refine(RefineArgs a, int n_tasks, in
     w.pitch = tile_pitch(a.N);
     w.pc = reinterpret_cast<double2*>(base);
     w.tg = base + (size_t)a.N * kWays * sizeof(double2);
-    w.ph = reinterpret_cast<double*>(base + (size_t)a.N * kWays * sizeof(double2) + (size_t)a.N * target_row_bytes(kFlat));
-    w.vs = w.ph + kPixBlock * w.pitch;
-    w.res = w.vs + kPixBlock * w.pitch;
+    w.tile = reinterpret_cast<double2*>(base + (size_t)a.N * kWays * sizeof(double2) + (size_t)a.N * target_row_bytes(kFlat));
+    w.res = reinterpret_cast<double*>(w.tile + kPixBlock * w.pitch);
     w.cand = g_cand + (size_t)gwarp * cap;
     w.es = g_es + (size_t)gwarp * cap;
 
