@@ -292,7 +292,8 @@ __device__ __forceinline__ double consistency_warp(const RefineArgs& a, const Wa
                     }
                     if (in) {
                         const unsigned dst = (unsigned)__cvta_generic_to_shared(e);
-                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(g.ras + py * a.W + px)
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst),
+                                     "l"(g.ras + (unsigned)(py * a.W + px))
                                      : "memory");
                     } else {
                         *reinterpret_cast<int*>(e) = -1;

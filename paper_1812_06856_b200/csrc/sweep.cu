@@ -154,6 +154,105 @@ __device__ __forceinline__ double sweep_chunk_fast(double cost, const double2* _
     return cost;
 }
 
+// One member-parallel sample for hypothesis depth d (fast path: the per-(hypothesis, target)
+// z, 1/z, K02 z, K12 z precomputed), bit-identical to sweep_chunk_fast's.
+__device__ __forceinline__ float sample_fast(const Cam& rc, const Cam& tc, const float4* __restrict__ timg, int W, int H,
+                                             double d, double z, double rz, double kz0, double kz1, double rx,
+                                             double ry, float4 ref, float T) {
+    if (!(z > 0)) return T;
+    const double hx = tc.K[0] * ((d * rx - rc.t[0]) + tc.t[0]) + kz0;
+    const double hy = tc.K[4] * ((d * ry - rc.t[1]) + tc.t[1]) + kz1;
+    const double qx = hx * rz, qy = hy * rz;
+    const double u = __fma_rn(__fma_rn(-qx, z, hx), rz, qx);
+    const double v = __fma_rn(__fma_rn(-qy, z, hy), rz, qy);
+    return tssd_at(timg, W, H, u, v, ref, T);
+}
+
+constexpr int kGroup = 32;       // hypotheses per member-parallel pass
+constexpr int kTilePitch = 260;  // floats per tile row: 16-byte rows, conflict-free float4 folds
+
+// Block-wide argmin of (cost, depth) over the hypotheses in list[0, cnt) (or all `levels` when
+// list == nullptr), the reference's "ties -> smaller depth" order (sweep.hpp:128-133).
+__device__ int block_argmin(const double* s_P, const double* s_d, const int* list, int cnt, double* red_c,
+                            double* red_d, int* red_k) {
+    double bc = INFINITY, bd = INFINITY;
+    int bk = -1;
+    for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
+        const int k = list ? list[q] : q;
+        const double c = s_P[k], d = s_d[k];
+        if (bk < 0 || c < bc || (c == bc && d < bd)) {
+            bc = c;
+            bd = d;
+            bk = k;
+        }
+    }
+    for (int off = 16; off; off >>= 1) {
+        const double oc = __shfl_xor_sync(LFDG_FULL_MASK, bc, off);
+        const double od = __shfl_xor_sync(LFDG_FULL_MASK, bd, off);
+        const int ok = __shfl_xor_sync(LFDG_FULL_MASK, bk, off);
+        if (ok >= 0 && (bk < 0 || oc < bc || (oc == bc && od < bd))) {
+            bc = oc;
+            bd = od;
+            bk = ok;
+        }
+    }
+    const int warp = threadIdx.x >> 5, nwarps = (blockDim.x + 31) >> 5;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) {
+        red_c[warp] = bc;
+        red_d[warp] = bd;
+        red_k[warp] = bk;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < nwarps; ++w)
+            if (red_k[w] >= 0 && (bk < 0 || red_c[w] < bc || (red_c[w] == bc && red_d[w] < bd))) {
+                bc = red_c[w];
+                bd = red_d[w];
+                bk = red_k[w];
+            }
+        red_k[0] = bk;
+    }
+    __syncthreads();
+    const int r = red_k[0];
+    __syncthreads();
+    return r;
+}
+
+// Ordered block compaction: list <- the k in [0, levels) with keep(k); returns the count.
+template <typename Pred>
+__device__ int block_compact(int levels, int* list, int* s_cnt, Pred keep) {
+    int base = 0;
+    for (int k0 = 0; k0 < levels; k0 += blockDim.x) {
+        const int k = k0 + threadIdx.x;
+        const bool f = k < levels && keep(k);
+        const unsigned m = __ballot_sync(LFDG_FULL_MASK, f);
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        if (lane == 0) s_cnt[warp] = __popc(m);
+        __syncthreads();
+        int off = base;
+        for (int w = 0; w < warp; ++w) off += s_cnt[w];
+        int tot = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += s_cnt[w];
+        if (f) list[off + __popc(m & ((1u << lane) - 1u))] = k;
+        __syncthreads();
+        base += tot;
+    }
+    return base;
+}
+
+// sweep_view (sweep.hpp:112-139) for one (view, superpixel): one CTA, the depth hypotheses of
+// sample_inverse_depths in shared memory.  Exact pruning, same winner as the dense argmin:
+//   A  every hypothesis runs the reference's cost chain over the first target (one thread per
+//      hypothesis, rays / colours staged in shared memory);
+//   B  the hypothesis h* with the smallest partial cost completes its chain: B = cost(h*);
+//   C  the others continue target by target while their partial cost is <= B.  The chain adds
+//      non-negative terms, so with round-to-nearest each partial cost is <= the final one
+//      (fl(a + x) >= a for x >= 0, monotone in a): a partial cost > B proves cost > B >= the
+//      minimum, so that hypothesis can neither win nor tie.
+// B and C run member-parallel: each thread samples one member pixel for up to kGroup
+// hypotheses into a shared tile, then one thread per hypothesis folds the tile row in member
+// order — the same sequential FP64 chain, sample by sample, as sweep_cost (sweep.hpp:85-107).
 template <bool kIdR, bool kCanonK>
 __global__ void __launch_bounds__(256) k_sweep(const float4* __restrict__ lab, int W, int H, int nsp, int v0,
                                                const Cam* __restrict__ cams, const int* __restrict__ targets,
@@ -162,11 +261,21 @@ __global__ void __launch_bounds__(256) k_sweep(const float4* __restrict__ lab, i
                                                double inv_hi, double step, float T, uint64_t seed,
                                                double4* planes) {
     extern __shared__ __align__(16) unsigned char smem[];
+    // [staging / tile union][cams][s_d][s_P][list]
+    constexpr size_t kUnion = kSweepCap * (sizeof(double2) + sizeof(float4)) > kGroup * kTilePitch * sizeof(float)
+                                  ? kSweepCap * (sizeof(double2) + sizeof(float4))
+                                  : kGroup * kTilePitch * sizeof(float);
     double2* s_ray = reinterpret_cast<double2*>(smem);
     float4* s_ref = reinterpret_cast<float4*>(smem + kSweepCap * sizeof(double2));
-    Cam* s_cam = reinterpret_cast<Cam*>(smem + kSweepCap * (sizeof(double2) + sizeof(float4)));
-    __shared__ double red_c[32];
-    __shared__ double red_d[32];
+    float* s_tile = reinterpret_cast<float*>(smem);
+    Cam* s_cam = reinterpret_cast<Cam*>(smem + kUnion);
+    double* s_d = reinterpret_cast<double*>(smem + kUnion + (size_t)(n_targets + 1) * sizeof(Cam));
+    double* s_P = s_d + levels;
+    int* s_list = reinterpret_cast<int*>(s_P + levels);
+    __shared__ double red_c[32], red_d[32];
+    __shared__ int red_k[32];
+    __shared__ double g_d[kGroup], g_z[kGroup], g_rz[kGroup], g_kz0[kGroup], g_kz1[kGroup];
+    __shared__ int g_h[kGroup];
 
     const int sp = blockIdx.x;
     const int view = v0 + blockIdx.y;
@@ -180,91 +289,140 @@ __global__ void __launch_bounds__(256) k_sweep(const float4* __restrict__ lab, i
     __syncthreads();
     const Cam& rc = s_cam[0];
 
-    auto load_chunk = [&](int c0) {
-        const int cn = min(kSweepCap, n - c0);
-        for (int i = threadIdx.x; i < cn; i += blockDim.x) {
-            const int p = mem[c0 + i];
-            const int x = p % W, y = p / W;
-            double rx, ry;
-            cam_ray(rc, (double)x, (double)y, rx, ry);
-            s_ray[i] = make_double2(rx, ry);
-            s_ref[i] = rimg[p];
-        }
-    };
-
+    // ---- A: hypotheses (sample_inverse_depths, geometry.hpp:116-130) and the first target
     const uint64_t s0 = derive_stream_state(seed, (uint64_t)view, (uint64_t)sp);
-    // Hypotheses of this thread: k = threadIdx.x, + blockDim.x, ...  (uniform trip count so the
-    // block-wide chunk loads below stay convergent).
     const int per = (levels + blockDim.x - 1) / blockDim.x;
-    double best_c = 0, best_d = 0;
-    bool have = false;
     for (int r = 0; r < per; ++r) {
         const int k = r * blockDim.x + threadIdx.x;
         const bool active = k < levels;
         double d = 0;
         if (active) {
-            // sample_inverse_depths (geometry.hpp:116-130)
             double inv = inv_lo + step * k + u64_to_unit(splitmix_at(s0, (uint64_t)k)) * step;
             if (inv > inv_hi) inv = inv_hi;
             d = 1.0 / inv;
         }
         double cost = 0;
-        for (int ti = 0; ti < n_targets; ++ti) {
-            const Cam& tc = s_cam[ti + 1];
-            const float4* timg = lab + (size_t)tg[ti] * hw;
+        if (n_targets > 0) {
+            const Cam& tc = s_cam[1];
+            const float4* timg = lab + (size_t)tg[0] * hw;
             for (int c0 = 0; c0 < n; c0 += kSweepCap) {
-                if (n > kSweepCap || (ti == 0 && c0 == 0 && r == 0)) {
+                if (n > kSweepCap || (c0 == 0 && r == 0)) {
                     __syncthreads();
-                    load_chunk(c0);
+                    const int cn = min(kSweepCap, n - c0);
+                    for (int i = threadIdx.x; i < cn; i += blockDim.x) {
+                        const int p = mem[c0 + i];
+                        double rx, ry;
+                        cam_ray(rc, (double)(p % W), (double)(p / W), rx, ry);
+                        s_ray[i] = make_double2(rx, ry);
+                        s_ref[i] = rimg[p];
+                    }
                     __syncthreads();
                 }
                 if (!active) continue;
                 const int cn = min(kSweepCap, n - c0);
                 if (kIdR && kCanonK) {
                     cost = sweep_chunk_fast(cost, s_ray, s_ref, cn, timg, W, H, d, rc, tc, T);
-                    continue;
-                }
-                for (int i = 0; i < cn; ++i) {
-                    const double2 ray = s_ray[i];
-                    const float t = sweep_sample<kIdR, kCanonK>(rc, tc, timg, W, H, d, ray.x, ray.y, s_ref[i], T);
-                    cost += (double)t;
+                } else {
+                    for (int i = 0; i < cn; ++i) {
+                        const double2 ray = s_ray[i];
+                        cost += (double)sweep_sample<kIdR, kCanonK>(rc, tc, timg, W, H, d, ray.x, ray.y, s_ref[i], T);
+                    }
                 }
             }
         }
-        if (active && (!have || cost < best_c || (cost == best_c && d < best_d))) {
-            best_c = cost;
-            best_d = d;
-            have = true;
+        if (active) {
+            s_d[k] = d;
+            s_P[k] = cost;
         }
-    }
-    if (!have) {
-        best_c = INFINITY;
-        best_d = INFINITY;
-    }
-    // block argmin on (cost, depth)
-    for (int off = 16; off; off >>= 1) {
-        const double oc = __shfl_xor_sync(LFDG_FULL_MASK, best_c, off);
-        const double od = __shfl_xor_sync(LFDG_FULL_MASK, best_d, off);
-        if (oc < best_c || (oc == best_c && od < best_d)) {
-            best_c = oc;
-            best_d = od;
-        }
-    }
-    const int warp = threadIdx.x >> 5, nwarps = (blockDim.x + 31) >> 5;
-    if ((threadIdx.x & 31) == 0) {
-        red_c[warp] = best_c;
-        red_d[warp] = best_d;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        double bc = red_c[0], bd = red_d[0];
-        for (int w = 1; w < nwarps; ++w)
-            if (red_c[w] < bc || (red_c[w] == bc && red_d[w] < bd)) {
-                bc = red_c[w];
-                bd = red_d[w];
+
+    // Continue the chains of list[0, cnt) over targets [t_begin, n_targets), pruning after
+    // each target (prune: keep only partial cost <= B).  Returns the surviving count.
+    auto advance = [&](int cnt, int t_begin, bool prune, double B) -> int {
+        for (int ti = t_begin; ti < n_targets && cnt > 0; ++ti) {
+            const Cam& tc = s_cam[ti + 1];
+            const float4* timg = lab + (size_t)tg[ti] * hw;
+            for (int g0 = 0; g0 < cnt; g0 += kGroup) {
+                const int gn = min(kGroup, cnt - g0);
+                if (threadIdx.x < gn) {
+                    const int h = s_list[g0 + threadIdx.x];
+                    const double d = s_d[h];
+                    const double z = (d - rc.t[2]) + tc.t[2];
+                    g_h[threadIdx.x] = h;
+                    g_d[threadIdx.x] = d;
+                    g_z[threadIdx.x] = z;
+                    g_rz[threadIdx.x] = 1.0 / z;
+                    g_kz0[threadIdx.x] = tc.K[2] * z;
+                    g_kz1[threadIdx.x] = tc.K[5] * z;
+                }
+                double acc = threadIdx.x < gn ? s_P[s_list[g0 + threadIdx.x]] : 0.0;
+                for (int c0 = 0; c0 < n; c0 += blockDim.x) {
+                    const int cn = min((int)blockDim.x, n - c0);
+                    __syncthreads();
+                    if ((int)threadIdx.x < cn) {
+                        const int p = mem[c0 + threadIdx.x];
+                        double rx, ry;
+                        cam_ray(rc, (double)(p % W), (double)(p / W), rx, ry);
+                        const float4 ref = rimg[p];
+                        for (int gi = 0; gi < gn; ++gi) {
+                            float val;
+                            if (kIdR && kCanonK)
+                                val = sample_fast(rc, tc, timg, W, H, g_d[gi], g_z[gi], g_rz[gi], g_kz0[gi], g_kz1[gi],
+                                                  rx, ry, ref, T);
+                            else
+                                val = sweep_sample<kIdR, kCanonK>(rc, tc, timg, W, H, g_d[gi], rx, ry, ref, T);
+                            s_tile[gi * kTilePitch + threadIdx.x] = val;
+                        }
+                    }
+                    __syncthreads();
+                    if ((int)threadIdx.x < gn) {
+                        const float* row = s_tile + threadIdx.x * kTilePitch;
+                        int jj = 0;
+                        for (; jj + 4 <= cn; jj += 4) {
+                            const float4 q = *reinterpret_cast<const float4*>(row + jj);
+                            acc += (double)q.x;
+                            acc += (double)q.y;
+                            acc += (double)q.z;
+                            acc += (double)q.w;
+                        }
+                        for (; jj < cn; ++jj) acc += (double)row[jj];
+                    }
+                }
+                if ((int)threadIdx.x < gn) s_P[g_h[threadIdx.x]] = acc;
+                __syncthreads();
             }
-        planes[(size_t)view * nsp + sp] = make_double4(bd, 0.0, 0.0, -1.0);
+            if (prune) {
+                // keep list members whose partial cost is still <= B (ordered, in place)
+                int* tmp = reinterpret_cast<int*>(s_tile);  // tile is free here
+                for (int q = threadIdx.x; q < cnt; q += blockDim.x) tmp[q] = s_list[q];
+                __syncthreads();
+                cnt = block_compact(cnt, s_list, red_k, [&](int q) { return s_P[tmp[q]] <= B; });
+                for (int q = threadIdx.x; q < cnt; q += blockDim.x) s_list[q] = tmp[s_list[q]];
+                __syncthreads();
+            }
+        }
+        return cnt;
+    };
+
+    int best;
+    if (n_targets <= 1) {
+        best = block_argmin(s_P, s_d, nullptr, levels, red_c, red_d, red_k);
+    } else {
+        // ---- B: complete the chain of the best partial hypothesis
+        const int hs = block_argmin(s_P, s_d, nullptr, levels, red_c, red_d, red_k);
+        if (threadIdx.x == 0) s_list[0] = hs;
+        __syncthreads();
+        advance(1, 1, false, 0.0);
+        const double B = s_P[hs];
+        // ---- C: the others, pruned against B after every target
+        int cnt = block_compact(levels, s_list, red_k, [&](int k) { return k != hs && s_P[k] <= B; });
+        cnt = advance(cnt, 1, true, B);
+        if (threadIdx.x == 0) s_list[cnt] = hs;
+        __syncthreads();
+        best = block_argmin(s_P, s_d, s_list, cnt + 1, red_c, red_d, red_k);
     }
+    if (threadIdx.x == 0) planes[(size_t)view * nsp + sp] = make_double4(s_d[best], 0.0, 0.0, -1.0);
 }
 
 // rasterize (sweep.hpp:44-63), one thread per pixel of views [v0, v0+n).
@@ -319,6 +477,8 @@ std::vector<int> matching_views(const Ctx& c, int view, int max_neighbors) {
 
 void sweep_views(Ctx& c, int v0, int n, const lfdg_sweep_params& p, uint64_t seed) {
     if (p.levels < 2) throw Error(LFDG_INVALID_PARAMS, "sweep levels must be >= 2");
+    // the hypotheses of one superpixel live in shared memory (and the prune list in the tile)
+    if (p.levels > 4096) throw Error(LFDG_INVALID_PARAMS, "sweep levels > 4096 are not supported");
     if (!(p.tssd_threshold > 0)) throw Error(LFDG_INVALID_PARAMS, "tssd threshold must be > 0");
     if (!(0 < c.d_min && c.d_min < c.d_max)) throw Error(LFDG_INVARIANT, "depth range requires 0 < d_min < d_max");
     if (v0 < 0 || n < 0 || v0 + n > c.V) throw Error(LFDG_STATE, "view range out of bounds");
@@ -337,8 +497,9 @@ void sweep_views(Ctx& c, int v0, int n, const lfdg_sweep_params& p, uint64_t see
     const double inv_lo = 1.0 / c.d_max;
     const double inv_hi = 1.0 / c.d_min;
     const double step = (inv_hi - inv_lo) / (p.levels - 1);
-    const int threads = std::min(256, (p.levels + 31) / 32 * 32);
-    const size_t smem = kSweepCap * (sizeof(double2) + sizeof(float4)) + (size_t)(nt + 1) * sizeof(Cam);
+    const int threads = 256;
+    const size_t smem = std::max(kSweepCap * (sizeof(double2) + sizeof(float4)), kGroup * kTilePitch * sizeof(float)) +
+                        (size_t)(nt + 1) * sizeof(Cam) + (size_t)p.levels * (2 * sizeof(double) + sizeof(int));
     dim3 grid(c.nsp, n);
     auto launch = [&](auto kernel) {
         LFDG_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
