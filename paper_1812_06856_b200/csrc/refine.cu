@@ -436,12 +436,13 @@ __device__ __forceinline__ double consistency_warp(const RefineArgs& a, const Wa
 // candidates are evaluated as in the reference.  init: cand[0] is the current plane and its
 // energy initialises e_cur (refine.hpp:277).
 template <bool kIdR, bool kCanonK, bool kFlat>
-__device__ __forceinline__ void greedy(const RefineArgs& a, const WarpSmem& w, int n, int v, int sp, int m0, int n_members,
-                       bool init, double& e_cur, double4& current, unsigned& accepted,
-                       unsigned long long& pix_evals, unsigned& cand_evals) {
+__device__ __forceinline__ void greedy(const RefineArgs& a, const WarpSmem& w, int base, int n, int v, int sp, int m0,
+                                       int n_members, bool init, double& e_cur, double4& current, unsigned& accepted,
+                                       unsigned long long& pix_evals, unsigned& cand_evals) {
     const int lane = threadIdx.x & 31;
     const bool prune = a.use_s && a.use_c;
-    int next = 0;
+    int next = base;
+    n += base;
     while (next < n) {
         // next candidate that survives the prune test (ordered ballot scan)
         const int idx = next + lane;
@@ -450,7 +451,8 @@ __device__ __forceinline__ void greedy(const RefineArgs& a, const WarpSmem& w, i
         // O_t = eta (1 - min_nb_sim) or 0), padded by 2^-30 against rounding, also prunes: a
         // candidate with E_s m_task <= e_cur has E <= e_cur and is never accepted, so the winner
         // and the accepted count are the reference's; only non-accepted evaluations are skipped.
-        const bool pass = idx < n && (init || !prune || w.es[idx] * w.m_task > e_cur);
+        // es = -inf marks a repeat of an earlier plane of this task (mark_repeats).
+        const bool pass = idx < n && w.es[idx] != -INFINITY && (init || !prune || w.es[idx] * w.m_task > e_cur);
         const unsigned m = __ballot_sync(LFDG_FULL_MASK, pass);
         if (!m) {
             next += 32;
@@ -479,10 +481,36 @@ __device__ __forceinline__ void greedy(const RefineArgs& a, const WarpSmem& w, i
     __syncwarp();
 }
 
-// es of cand[0, n): 4 candidates per warp step (8 ring lanes each).
-__device__ void smoothness_all(const RefineArgs& a, const WarpSmem& w, int n, int v, int sp) {
+// A candidate bit-identical to a plane met earlier in this task (the initial plane cand[0], or
+// any earlier candidate, evaluated or pruned) has that plane's energy, which is <= the running
+// best at that point and hence <= e_cur now: it can never be accepted (this subsumes the
+// reference's skip of the current plane, refine.hpp:292).  Marks cand[lo, hi) repeats with
+// es = -inf; the others get es = 0 when there is no smoothness term.
+__device__ void mark_repeats(const RefineArgs& a, const WarpSmem& w, int lo, int hi) {
     const int lane = threadIdx.x & 31;
-    for (int b = 0; b < n; b += 4) {
+    for (int c = lo + lane; c < hi; c += 32) {
+        const double4 p = w.cand[c];
+        bool rep = false;
+        for (int c2 = 0; c2 < c && !rep; ++c2) {
+            const double4 q = w.cand[c2];
+            rep = __double_as_longlong(p.x) == __double_as_longlong(q.x) &&
+                  __double_as_longlong(p.y) == __double_as_longlong(q.y) &&
+                  __double_as_longlong(p.z) == __double_as_longlong(q.z) &&
+                  __double_as_longlong(p.w) == __double_as_longlong(q.w);
+        }
+        if (rep)
+            w.es[c] = -INFINITY;
+        else if (!a.use_s)
+            w.es[c] = 0.0;
+    }
+    __syncwarp();
+}
+
+// es of cand[base, base + n): 4 candidates per warp step (8 ring lanes each).
+__device__ void smoothness_all(const RefineArgs& a, const WarpSmem& w, int base, int n, int v, int sp) {
+    const int lane = threadIdx.x & 31;
+    n += base;
+    for (int b = base; b < n; b += 4) {
         const int ci = b + (lane >> 3);
         const bool active = ci < n;
         const double4 p = active ? w.cand[ci] : make_double4(1, 0, 0, -1);
@@ -567,8 +595,10 @@ __global__ void __launch_bounds__(128, LFDG_REFINE_MIN_BLOCKS) k_refine(RefineAr
         // ---- e_cur = energy(current) (refine.hpp:277)
         if (lane == 0) w.cand[0] = cur0;
         __syncwarp();
-        if (a.use_s) smoothness_all(a, w, 1, v, sp);
-        greedy<kIdR, kCanonK, kFlat>(a, w, 1, v, sp, m0, n_members, true, e_cur, current, accepted, pix_evals, cand_evals);
+        if (a.use_s) smoothness_all(a, w, 0, 1, v, sp);
+        mark_repeats(a, w, 0, 1);
+        greedy<kIdR, kCanonK, kFlat>(a, w, 0, 1, v, sp, m0, n_members, true, e_cur, current, accepted, pix_evals,
+                                     cand_evals);
 
         // ---- phase A: grid_neighbors(Kernel) order (superpixel.hpp:318-343), re-anchored
         const int gx = sp % a.gw, gy = sp / a.gw;
@@ -608,12 +638,14 @@ __global__ void __launch_bounds__(128, LFDG_REFINE_MIN_BLOCKS) k_refine(RefineAr
                 }
             }
             const unsigned m = __ballot_sync(LFDG_FULL_MASK, ok);
-            if (ok) w.cand[n_cand + __popc(m & ((1u << lane) - 1u))] = cand;
+            if (ok) w.cand[1 + n_cand + __popc(m & ((1u << lane) - 1u))] = cand;
             n_cand += __popc(m);
         }
         __syncwarp();
-        if (a.use_s) smoothness_all(a, w, n_cand, v, sp);
-        greedy<kIdR, kCanonK, kFlat>(a, w, n_cand, v, sp, m0, n_members, false, e_cur, current, accepted, pix_evals, cand_evals);
+        if (a.use_s) smoothness_all(a, w, 1, n_cand, v, sp);
+        mark_repeats(a, w, 1, 1 + n_cand);
+        greedy<kIdR, kCanonK, kFlat>(a, w, 1, n_cand, v, sp, m0, n_members, false, e_cur, current, accepted, pix_evals,
+                                     cand_evals);
 
         // ---- phase B: normal_candidates (refine.hpp:213-242) at the phase-A depth
         {
@@ -653,11 +685,13 @@ __global__ void __launch_bounds__(128, LFDG_REFINE_MIN_BLOCKS) k_refine(RefineAr
                 }
             }
             const unsigned m = __ballot_sync(LFDG_FULL_MASK, okn);
-            if (okn) w.cand[__popc(m & ((1u << lane) - 1u))] = nc;
+            if (okn) w.cand[1 + n_cand + __popc(m & ((1u << lane) - 1u))] = nc;
             __syncwarp();
             const int nn = __popc(m);
-            if (a.use_s) smoothness_all(a, w, nn, v, sp);
-            greedy<kIdR, kCanonK, kFlat>(a, w, nn, v, sp, m0, n_members, false, e_cur, current, accepted, pix_evals, cand_evals);
+            if (a.use_s) smoothness_all(a, w, 1 + n_cand, nn, v, sp);
+            mark_repeats(a, w, 1 + n_cand, 1 + n_cand + nn);
+            greedy<kIdR, kCanonK, kFlat>(a, w, 1 + n_cand, nn, v, sp, m0, n_members, false, e_cur, current, accepted,
+                                         pix_evals, cand_evals);
         }
         if (lane == 0) a.out[vs + sp] = current;
         accepted_total += accepted;
@@ -832,7 +866,7 @@ void refine_iteration(Ctx& c, int l) {
     a.n_slots = 8 + 8 * a.per_dir;
     a.counters = c.counters.p;
     if (a.N > kMaxTargets) throw Error(LFDG_INVALID_PARAMS, "too many matching views (max 64)");
-    const int cap = std::max(a.n_slots, 8) + 1;
+    const int cap = 1 + a.n_slots + 8;  // cand[0] = the task's plane, then phase A, then phase B
     bool flat = c.identity_rot && c.canonical_k;
     for (const lfdg_camera& k : c.cams)
         flat = flat && k.t[2] == 0.0 && k.K[0] == c.cams[0].K[0] && k.K[2] == c.cams[0].K[2] &&
