@@ -57,6 +57,7 @@ struct RefineArgs {
     int kernel_px, kernel_step, radius_sp, per_dir, n_slots;
     double uK00, uK02, uK11, uK12;  // the shared K of a kFlat view set
     int row_inv;                    // kFlat and every rel_trans.y == 0: target rows are view-invariant
+                                    // (selects kFlat == 2)
     unsigned long long* counters;
 };
 
@@ -222,7 +223,7 @@ __device__ __forceinline__ double photo_weight(const RefineArgs& a, const WarpSm
 // go to a shared tile, then lane t folds target t's column in member order — the reference's
 // sequential photo_sum / vis_sum / x_count / y_nonempty of pair_stats (refine.hpp:127-163),
 // bit for bit.  Finally V + O are summed in target order (refine.hpp:193-198).
-template <bool kIdR, bool kCanonK, bool kFlat>
+template <bool kIdR, bool kCanonK, int kFlat>
 __device__ __forceinline__ double consistency_warp(const RefineArgs& a, const WarpSmem& w, int v, int sp, double4 p,
                                                    int m0, int n) {
     const int lane = threadIdx.x & 31;
@@ -266,7 +267,7 @@ __device__ __forceinline__ double consistency_warp(const RefineArgs& a, const Wa
                 f_inv = 1.0 / sv2;
                 f_kz0 = a.uK02 * sv2;
                 f_kz1 = a.uK12 * sv2;
-                if (a.row_inv) {  // every T.y = 0 (linear rig): the target row is the same for all
+                if (kFlat == 2) {  // every T.y = 0 (linear rig): the target row is the same for all
                     const double hy = a.uK11 * sv1 + f_kz1;
                     if (!fast_lround(hy * f_inv, f_py)) f_py = lround_int(hy / sv2);
                 }
@@ -284,7 +285,7 @@ __device__ __forceinline__ double consistency_warp(const RefineArgs& a, const Wa
                     if (ok) {
                         const double hx = a.uK00 * (sv0 + g.T0) + f_kz0;
                         if (!fast_lround(hx * f_inv, px)) px = lround_int(hx / sv2);
-                        if (!a.row_inv) {
+                        if (kFlat != 2) {
                             const double hy = a.uK11 * (sv1 + g.T1) + f_kz1;
                             if (!fast_lround(hy * f_inv, py)) py = lround_int(hy / sv2);
                         }
@@ -435,7 +436,7 @@ __device__ __forceinline__ double consistency_warp(const RefineArgs& a, const Wa
 // candidate in index order with the running prune E_s (1 + eta) <= e_cur: the same
 // candidates are evaluated as in the reference.  init: cand[0] is the current plane and its
 // energy initialises e_cur (refine.hpp:277).
-template <bool kIdR, bool kCanonK, bool kFlat>
+template <bool kIdR, bool kCanonK, int kFlat>
 __device__ __forceinline__ void greedy(const RefineArgs& a, const WarpSmem& w, int base, int n, int v, int sp, int m0,
                                        int n_members, bool init, double& e_cur, double4& current, unsigned& accepted,
                                        unsigned long long& pix_evals, unsigned& cand_evals) {
@@ -522,7 +523,7 @@ __device__ void smoothness_all(const RefineArgs& a, const WarpSmem& w, int base,
 
 // Persistent kernel: each warp pulls (view, superpixel) tasks from a global counter and runs
 // refine_iteration's task body (refine.hpp:269-320) for it.
-template <bool kIdR, bool kCanonK, bool kFlat>
+template <bool kIdR, bool kCanonK, int kFlat>
 #ifndef LFDG_REFINE_MIN_BLOCKS
 #define LFDG_REFINE_MIN_BLOCKS 8
 #endif
@@ -905,15 +906,18 @@ void refine_iteration(Ctx& c, int l) {
             a.uK02 = c.cams[0].K[2];
             a.uK11 = c.cams[0].K[4];
             a.uK12 = c.cams[0].K[5];
-            launch(k_refine<true, true, true>);
+            if (a.row_inv)
+                launch(k_refine<true, true, 2>);
+            else
+                launch(k_refine<true, true, 1>);
         } else if (c.identity_rot && c.canonical_k) {
-            launch(k_refine<true, true, false>);
+            launch(k_refine<true, true, 0>);
         } else if (c.identity_rot) {
-            launch(k_refine<true, false, false>);
+            launch(k_refine<true, false, 0>);
         } else if (c.canonical_k) {
-            launch(k_refine<false, true, false>);
+            launch(k_refine<false, true, 0>);
         } else {
-            launch(k_refine<false, false, false>);
+            launch(k_refine<false, false, 0>);
         }
         LFDG_LAUNCHED(&c);
         LFDG_CUDA_CHECK(cudaMemcpyAsync(c.planes.p + (size_t)rv0 * c.nsp, c.planes_next.p + (size_t)rv0 * c.nsp,
