@@ -75,6 +75,9 @@ __device__ __forceinline__ int lround_int(double x) {
     return (int)(unsigned)(unsigned long long)r;
 }
 
+// lround(h / z) the slow way (division, then lround), out of line: fast_lround's rare fallback.
+__device__ __noinline__ int lround_div(double h, double z) { return lround_int(h / z); }
+
 // depth_consistency (refine.hpp:34-37)
 __device__ __forceinline__ double depth_consistency(double d1, double d2, double two_sigma2) {
     const double r = 1.0 / d1 - 1.0 / d2;
@@ -138,8 +141,8 @@ __device__ __forceinline__ bool fast_lround(double q, int& out) {
 }
 
 // Per-warp shared-memory slice.  Candidate planes / upper bounds live in a per-warp global
-// scratch row (L1-resident); the per-task target table, the photo-weight cache and the
-// pixel-term tile are shared memory.
+// scratch row (L1-resident); the per-task target table, the per-pixel geometry of the current
+// pixel chunk, the photo-weight cache and the per-target results are shared memory.
 struct TargetRow {   // one matching view of the task (refine.hpp:116-118, 46-47)
     double R[9];
     double T[3];
@@ -151,41 +154,38 @@ struct TargetFlat {  // kFlat: R = I, t.z = 0 and the shared K make everything b
     const int4* ras;
     const void* pad;
 };
+// Target-independent part of pair_stats' transfer for one member pixel (refine.hpp:131-137):
+// s v, and for kFlat (every R = I, every t.z = 0, one shared K) z = s, 1/z, K02 z, K12 z and,
+// for a linear rig, the rounded target row.
+struct PixGeo {
+    double sv0, sv1, sv2;
+    double f_inv, f_kz0, f_kz1;
+    int f_py;
+    int ok;
+};
 struct WarpSmem {
     double4* cand;  // [cap]   (global scratch)
     double* es;     // [cap]   (global scratch)
     void* tg;       // [N] TargetRow, or TargetFlat for kFlat
-    double2* pc;    // [N][kWays] photo-weight cache: (weight, raster word of the target label)
-    double2* tile;  // [16][pitch] per (pixel j, target tt): (photo term: weight, or -1 = no sample;
-                    // visibility term: Gaussian (visible), -1 (occluded), -2 (no target depth));
-                    // kFlat first stages the pixel's raster record (label word, depth, 1/depth) there
-    double* res;    // [N] V + O per target
+    PixGeo* geo;    // [32] geometry of the current pixel chunk (one entry per lane)
+    double2* pc;    // [kWays][cw] lane-private photo-weight cache: (weight, raster word)
+    double* res;    // [2][N] V + O per target, per candidate slot
     double m_task;  // upper bound of V_t + O_t for the current task
-    int pitch;
+    int cw;         // photo-cache row width: max(32, N)
 };
 constexpr int kMaxTargets = 64;
-constexpr int kPixBlock = 16;  // member pixels per tile (a half-warp each; the halves split the targets)
-constexpr int kWays = 8;       // photo-cache slots per target: (gx & 3, gy & 1) of the target superpixel
+constexpr int kWays = 4;  // photo-cache slots per (lane, target)
 
-__host__ __device__ inline int tile_pitch(int N) {
-    const int nr = N < 32 ? N : 32;
-    return (nr & 1) ? nr : nr + 1;  // odd pitch: conflict-free column reads
-}
+__host__ __device__ inline int cache_width(int N) { return N > 32 ? N : 32; }
 __host__ __device__ inline size_t target_row_bytes(bool flat) { return flat ? sizeof(TargetFlat) : sizeof(TargetRow); }
 __host__ __device__ inline size_t warp_smem_bytes(int N, bool flat) {
-    const size_t b = (size_t)N * kWays * sizeof(double2) + (size_t)N * target_row_bytes(flat) +
-                     2 * kPixBlock * (size_t)tile_pitch(N) * sizeof(double) + (size_t)N * sizeof(double);
+    const size_t b = (size_t)kWays * cache_width(N) * sizeof(double2) + (size_t)N * target_row_bytes(flat) +
+                     32 * sizeof(PixGeo) + 2 * (size_t)N * sizeof(double);
     return (b + 127) & ~(size_t)127;
 }
 
-// Photo weight exp(-|c_ref - c_t(label)|^2 / (2 alpha^2)) of pair_stats (refine.hpp:146-150)
-// is a pure function of the task's reference colour and the target label, so the reference's
-// one-entry label cache (cached_label / cached_w) generalises to a per-task, per-warp cache:
-// kWays direct-mapped slots per target, keyed by the raster word (label | slot << 28).  A
-// lane that misses computes the weight itself (same expression, same bits) and one lane per
-// slot writes it back; hits read the identical value.  am: the converged lanes calling it.
-// The cache-miss path, out of line so that its registers do not weigh on the hot loop; the
-// operands are re-read from memory (L1) instead of being kept live.
+// The cache-miss path of the photo weight, out of line so that its registers do not weigh on the
+// hot loop; the operands are re-read from memory (L1) instead of being kept live.
 __device__ __noinline__ double photo_miss(const int* target, const float4* ref, const float4* color, int nsp, int label,
                                           double inv_two_alpha2) {
     const float4 rc = *ref;
@@ -193,289 +193,234 @@ __device__ __noinline__ double photo_miss(const int* target, const float4* ref, 
     return libm::exp_nonpos(-(double)color_dist2(rc.x, rc.y, rc.z, c.x, c.y, c.z) * inv_two_alpha2);
 }
 
-__device__ __forceinline__ double photo_weight(const RefineArgs& a, const WarpSmem& w, int v, int sp, int tslot,
-                                               int word, bool valid, unsigned am) {
-    const int slot = tslot * kWays + ((unsigned)word >> 28);
-    double ph = -1.0;
-    bool hit = true;
-    if (valid) {
-        const double2 e = w.pc[slot];
-        hit = __double2loint(e.y) == word;
-        ph = e.x;
-    }
-    const unsigned miss = __ballot_sync(am, !hit);
-    if (miss) {
-        if (!hit) {
-            ph = photo_miss(a.targets + (size_t)v * a.N + tslot, a.color + (size_t)v * a.nsp + sp, a.color, a.nsp,
-                            word & 0x0FFFFFFF, a.inv_two_alpha2);
-            const unsigned peers = __match_any_sync(miss, slot);
-            if ((peers & ((1u << (threadIdx.x & 31)) - 1u)) == 0)
-                w.pc[slot] = make_double2(ph, __hiloint2double(-1, word));
+// Per-pixel geometry of member pixel i for plane p (refine.hpp:131-137).
+template <int kFlat>
+__device__ __forceinline__ PixGeo pixel_geo(const RefineArgs& a, const double2* mr, int i, int n, double4 p,
+                                            double plane_num) {
+    PixGeo q;
+    q.ok = 0;
+    q.sv0 = q.sv1 = q.sv2 = 0;
+    q.f_inv = q.f_kz0 = q.f_kz1 = 0;
+    q.f_py = -1;
+    if (i < n) {
+        const double2 r = mr[i];
+        const double denom = (p.y * r.x + p.z * r.y) + p.w;
+        if (!(fabs(denom) <= 1e-9)) {  // degenerate ray: invisible
+            const double s = plane_num / denom;
+            if (s > 0) {
+                q.ok = 1;
+                q.sv0 = s * r.x;
+                q.sv1 = s * r.y;
+                q.sv2 = s;
+            }
         }
-        __syncwarp(am);
     }
-    return ph;
+    if (kFlat && q.ok) {
+        q.f_inv = 1.0 / q.sv2;
+        q.f_kz0 = a.uK02 * q.sv2;
+        q.f_kz1 = a.uK12 * q.sv2;
+        if (kFlat == 2) {  // every T.y = 0 (linear rig): the target row is the same for all targets
+            const double hy = a.uK11 * q.sv1 + q.f_kz1;
+            if (!fast_lround(hy * q.f_inv, q.f_py)) q.f_py = lround_int(hy / q.sv2);
+        }
+    }
+    return q;
 }
 
-// consistency_term (refine.hpp:189-199) of plane p for task (v, sp), one warp.
-// Each half-warp owns the same 16 consecutive member pixels (coherent branches, coalesced ray
-// loads, neighbouring gathers); the halves take alternate targets.  Per-(pixel, target) terms
-// go to a shared tile, then lane t folds target t's column in member order — the reference's
-// sequential photo_sum / vis_sum / x_count / y_nonempty of pair_stats (refine.hpp:127-163),
-// bit for bit.  Finally V + O are summed in target order (refine.hpp:193-198).
+// consistency_term (refine.hpp:189-199) of up to two candidate planes of task (v, sp) at once.
+// Lanes are (candidate slot, target): with N <= 16 targets each half-warp evaluates its own
+// candidate (G = 16 lanes, lane = target), otherwise the whole warp evaluates one (G = 32, lanes
+// stride over the targets).  Each lane runs pair_stats (refine.hpp:111-172) for its target
+// exactly as the reference does — the member pixels in order, photo_sum / vis_sum / x_count /
+// y_nonempty accumulated sequentially in registers, the same one-entry label cache — so every
+// sum is bit-identical.  The target-independent geometry of each pixel chunk is computed once
+// per pixel (one lane per pixel) and broadcast through shared memory.  The label cache is backed
+// by a small lane-private cache of photo weights, which are pure functions of (task colour,
+// target, label) and so stay valid for the whole task.  V + O are summed in target order.
 template <bool kIdR, bool kCanonK, int kFlat>
-__device__ __forceinline__ double consistency_warp(const RefineArgs& a, const WarpSmem& w, int v, int sp, double4 p,
+__device__ __forceinline__ double consistency_pair(const RefineArgs& a, const WarpSmem& w, int v, int sp, double4 p,
                                                    int m0, int n) {
     const int lane = threadIdx.x & 31;
-    const int j = lane & (kPixBlock - 1);
-    const int half = lane >> 4;
     const int N = a.N;
     if (N == 0) return 1.0;
+    const int G = N <= 16 ? 16 : 32;
+    const int cs = lane / G;  // candidate slot
+    const int tl = lane % G;  // target lane
     const size_t hw = (size_t)a.W * a.H;
     const double2 cr = a.cray[(size_t)v * a.nsp + sp];
     const double ax = p.x * cr.x, ay = p.x * cr.y, az = p.x;
-    const double plane_num = (p.y * ax + p.z * ay) + p.w * az;
+    const double plane_num = (p.y * ax + p.z * ay) + p.w * az;  // plane.normal.dot(anchor)
     const double2* mr = a.mray + (size_t)v * hw + m0;
-    const int pitch = w.pitch;
-    for (int t0 = 0; t0 < N; t0 += 32) {
-        const int nr = min(32, N - t0);
+    const double occ = a.use_o ? a.eta * (1.0 - (double)a.min_nb_sim[(size_t)v * a.nsp + sp]) : 0.0;
+    const PixGeo* geo = w.geo + cs * G;
+    double* res = w.res + cs * N;
+    for (int t0 = 0; t0 < N; t0 += G) {
+        const int t = t0 + tl;
+        const bool act = t < N;
+        const int cslot = G == 16 ? lane : (act ? t : 0);  // this lane's photo-cache column
+        double T0 = 0, T1 = 0;
+        const int4* ras = nullptr;
+        if (kFlat && act) {
+            const TargetFlat& g = static_cast<const TargetFlat*>(w.tg)[t];
+            T0 = g.T0;
+            T1 = g.T1;
+            ras = g.ras;
+        }
         double photo_sum = 0, vis_sum = 0;
-        int neg = 0;             // fold lanes: tile entries that are not addends (-0.0)
-        unsigned occbits = 0;    // compute lanes: bit k = some pixel of target half + 2k occluded
-        for (int b = 0; b < n; b += kPixBlock) {
-            const int i = b + j;
-            bool ok = false;
-            double sv0 = 0, sv1 = 0, sv2 = 0;
-            if (i < n) {
-                const double2 r = mr[i];
-                const double denom = (p.y * r.x + p.z * r.y) + p.w;
-                if (!(fabs(denom) <= 1e-9)) {
-                    const double s = plane_num / denom;
-                    if (s > 0) {
-                        ok = true;
-                        sv0 = s * r.x;
-                        sv1 = s * r.y;
-                        sv2 = s;
-                    }
-                }
-            }
-            // kFlat (every R = I, every t.z = 0, one shared K): the target-frame z is s for every
-            // target, so 1/z and K02 z, K12 z are per-pixel constants.
-            double f_inv = 0, f_kz0 = 0, f_kz1 = 0;
-            int f_py = -1;
-            if (kFlat && ok) {
-                f_inv = 1.0 / sv2;
-                f_kz0 = a.uK02 * sv2;
-                f_kz1 = a.uK12 * sv2;
-                if (kFlat == 2) {  // every T.y = 0 (linear rig): the target row is the same for all
-                    const double hy = a.uK11 * sv1 + f_kz1;
-                    if (!fast_lround(hy * f_inv, f_py)) f_py = lround_int(hy / sv2);
-                }
-            }
-            if (kFlat) {
-                // Two phases so that the raster gathers of all of this lane's targets are in flight
-                // together: (1) project and start a 16-byte cp.async of each target's record into
-                // the tile (or mark it out of bounds), (2) wait, then turn each record into the
-                // (photo, visibility) pair in place.
-                for (int tt = half; tt < nr; tt += 2) {
-                    const TargetFlat& g = static_cast<const TargetFlat*>(w.tg)[t0 + tt];
-                    double2* e = &w.tile[j * pitch + tt];
-                    bool in = false;
-                    int px = 0, py = f_py;
-                    if (ok) {
-                        const double hx = a.uK00 * (sv0 + g.T0) + f_kz0;
-                        if (!fast_lround(hx * f_inv, px)) px = lround_int(hx / sv2);
-                        if (kFlat != 2) {
-                            const double hy = a.uK11 * (sv1 + g.T1) + f_kz1;
-                            if (!fast_lround(hy * f_inv, py)) py = lround_int(hy / sv2);
+        int x_count = 0;
+        bool y_nonempty = false;
+        int cached_word = -1;
+        double cached_w = 0;
+        for (int b = 0; b < n; b += G) {
+            w.geo[lane] = pixel_geo<kFlat>(a, mr, b + tl, n, p, plane_num);
+            __syncwarp();
+            const int cnt = min(G, n - b);
+            if (act) {
+                for (int jj = 0; jj < cnt; ++jj) {
+                    const PixGeo& q = geo[jj];
+                    if (!q.ok) continue;
+                    int px, py;
+                    double zt, inv_z;
+                    if (kFlat) {
+                        const double hx = a.uK00 * (q.sv0 + T0) + q.f_kz0;
+                        if (!fast_lround(hx * q.f_inv, px)) px = lround_div(hx, q.sv2);
+                        if (kFlat == 2) {
+                            py = q.f_py;
+                        } else {
+                            const double hy = a.uK11 * (q.sv1 + T1) + q.f_kz1;
+                            if (!fast_lround(hy * q.f_inv, py)) py = lround_div(hy, q.sv2);
                         }
-                        in = (unsigned)px < (unsigned)a.W && (unsigned)py < (unsigned)a.H;
-                    }
-                    if (in) {
-                        const unsigned dst = (unsigned)__cvta_generic_to_shared(e);
-                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst),
-                                     "l"(g.ras + (unsigned)(py * a.W + px))
-                                     : "memory");
+                        zt = q.sv2;
+                        inv_z = q.f_inv;
                     } else {
-                        *reinterpret_cast<int*>(e) = -1;
-                    }
-                }
-                asm volatile("cp.async.wait_all;\n" ::: "memory");
-                for (int tt = half; tt < nr; tt += 2) {
-                    double2* e = &w.tile[j * pitch + tt];
-                    const int4 r = *reinterpret_cast<const int4*>(e);
-                    const bool in = r.x >= 0;
-                    double vsv = -2.0;
-                    if (in) {
-                        const float td = __int_as_float(r.y);
-                        if (!(td <= 0)) {
-                            if (sv2 <= (double)td * (1.0 + 1e-6)) {
-                                const double rr = f_inv - __hiloint2double(r.w, r.z);
-                                vsv = libm::exp_nonpos(-rr * rr * a.inv_two_sigma2);
-                            } else {
-                                vsv = -1.0;
-                            }
+                        const TargetRow& g = static_cast<const TargetRow*>(w.tg)[t];
+                        double x0, x1, x2;
+                        if (kIdR) {
+                            x0 = q.sv0 + g.T[0];
+                            x1 = q.sv1 + g.T[1];
+                            x2 = q.sv2 + g.T[2];
+                        } else {
+                            x0 = ((g.R[0] * q.sv0 + g.R[1] * q.sv1) + g.R[2] * q.sv2) + g.T[0];
+                            x1 = ((g.R[3] * q.sv0 + g.R[4] * q.sv1) + g.R[5] * q.sv2) + g.T[1];
+                            x2 = ((g.R[6] * q.sv0 + g.R[7] * q.sv1) + g.R[8] * q.sv2) + g.T[2];
                         }
-                    }
-                    const unsigned am = __activemask();  // both halves, or the even half alone (odd nr)
-                    const double ph = photo_weight(a, w, v, sp, t0 + tt, r.x, in, am);
-                    occbits |= (vsv == -1.0 ? 1u : 0u) << (tt >> 1);
-                    *e = make_double2(in ? ph : -0.0, vsv >= 0 ? vsv : -0.0);
-                }
-            } else {
-            for (int tt = half; tt < nr; tt += 2) {
-                // target-frame z, 1/z and the rounded pixel (refine.hpp:138-145)
-                bool in = false;
-                double zt = 0, inv_z = 0;
-                int px = 0, py = 0;
-                const TargetRow& g = static_cast<const TargetRow*>(w.tg)[t0 + tt];
-                const int4* ras = g.ras;
-                if (ok) {
-                    double x0, x1, x2;
-                    if (kIdR) {
-                        x0 = sv0 + g.T[0];
-                        x1 = sv1 + g.T[1];
-                        x2 = sv2 + g.T[2];
-                    } else {
-                        x0 = ((g.R[0] * sv0 + g.R[1] * sv1) + g.R[2] * sv2) + g.T[0];
-                        x1 = ((g.R[3] * sv0 + g.R[4] * sv1) + g.R[5] * sv2) + g.T[1];
-                        x2 = ((g.R[6] * sv0 + g.R[7] * sv1) + g.R[8] * sv2) + g.T[2];
-                    }
-                    if (x2 > 0) {
+                        if (!(x2 > 0)) continue;  // behind the target camera
                         const double hx = kCanonK ? g.K00 * x0 + g.K02 * x2 : (g.K00 * x0 + g.K01 * x1) + g.K02 * x2;
                         const double hy = g.K11 * x1 + g.K12 * x2;
                         inv_z = 1.0 / x2;
-                        if (!fast_lround(hx * inv_z, px)) px = lround_int(hx / x2);
-                        if (!fast_lround(hy * inv_z, py)) py = lround_int(hy / x2);
-                        in = !(px < 0 || py < 0 || px >= a.W || py >= a.H);
+                        if (!fast_lround(hx * inv_z, px)) px = lround_div(hx, x2);
+                        if (!fast_lround(hy * inv_z, py)) py = lround_div(hy, x2);
                         zt = x2;
+                        ras = g.ras;
                     }
-                }
-                // tgrid.label(px, py) and snapshot.depth[t](px, py) (refine.hpp:146-152) in one
-                // 16-byte gather: (label word, depth, 1 / (double)depth)
-                int word = 0;
-                double vsv = -2.0;
-                if (in) {
-                    const int4 r = __ldg(&ras[py * a.W + px]);
-                    word = r.x;
-                    const float td = __int_as_float(r.y);
-                    if (!(td <= 0)) {
-                        if (zt <= (double)td * (1.0 + 1e-6)) {
-                            const double rr = inv_z - __hiloint2double(r.w, r.z);
-                            vsv = libm::exp_nonpos(-rr * rr * a.inv_two_sigma2);
+                    if ((unsigned)px >= (unsigned)a.W || (unsigned)py >= (unsigned)a.H) continue;
+                    // tgrid.label(px, py) and snapshot.depth[t](px, py) (refine.hpp:146-152) in one
+                    // 16-byte gather: (label word, depth, 1 / (double)depth)
+                    const int4 r = __ldg(ras + (unsigned)(py * a.W + px));
+                    if (r.x != cached_word) {  // refine.hpp:147-150
+                        const int way = (((unsigned)r.x >> 28) + 2 * ((unsigned)r.x >> 30)) & (kWays - 1);
+                        double2* e = &w.pc[way * w.cw + cslot];
+                        const double2 c = *e;
+                        if (__double2loint(c.y) == r.x) {
+                            cached_w = c.x;
                         } else {
-                            vsv = -1.0;
+                            cached_w = photo_miss(a.targets + (size_t)v * N + t, a.color + (size_t)v * a.nsp + sp,
+                                                  a.color, a.nsp, r.x & 0x0FFFFFFF, a.inv_two_alpha2);
+                            *e = make_double2(cached_w, __hiloint2double(-1, r.x));
                         }
+                        cached_word = r.x;
                     }
-                }
-                const unsigned am = __activemask();  // both halves, or the even half alone (odd nr)
-                const double ph = photo_weight(a, w, v, sp, t0 + tt, word, in, am);
-                occbits |= (vsv == -1.0 ? 1u : 0u) << (tt >> 1);
-                w.tile[j * pitch + tt] = make_double2(in ? ph : -0.0, vsv >= 0 ? vsv : -0.0);
-            }
-            }
-            __syncwarp();
-            // Fold in member order: pair_stats' sequential photo_sum / vis_sum (refine.hpp:
-            // 147-158).  The tile holds addends only — a pixel that adds nothing holds -0.0, an
-            // exact identity of these sums (non-negative terms from +0.0) — so the fold is a
-            // plain chain; the sign bit counts the non-visible entries (x_count) on the way.
-            // nr <= 16: the photo chain of target t runs on lane t and its visibility chain on
-            // lane 16 + t; otherwise lane t runs both.  Rows past the last member hold -0.0.
-            if (nr <= 16) {
-                const int tl = lane & 15;
-                const double* colp = reinterpret_cast<const double*>(w.tile + tl) + half;
-                if (tl < nr) {
-#pragma unroll
-                    for (int jj = 0; jj < kPixBlock; ++jj) {
-                        const double val = colp[2 * jj * pitch];
-                        vis_sum += val;  // photo_sum on the photo lanes (merged below)
-                        neg += (unsigned)__double2hiint(val) >> 31;
+                    photo_sum += cached_w;
+                    const float td = __int_as_float(r.y);
+                    if (td <= 0) continue;  // no target depth: not in X or Y
+                    if (zt <= (double)td * (1.0 + 1e-6)) {
+                        const double rr = inv_z - __hiloint2double(r.w, r.z);
+                        vis_sum += libm::exp_nonpos(-rr * rr * a.inv_two_sigma2);
+                        ++x_count;
+                    } else {
+                        y_nonempty = true;
                     }
-                }
-            } else if (lane < nr) {
-#pragma unroll 4
-                for (int jj = 0; jj < kPixBlock; ++jj) {
-                    const double2 e = w.tile[jj * pitch + lane];
-                    photo_sum += e.x;
-                    vis_sum += e.y;
-                    neg += (unsigned)__double2hiint(e.y) >> 31;
                 }
             }
             __syncwarp();
         }
-        if (nr <= 16) {
-            // lane t: its accumulator is photo_sum; take the visibility statistics from lane 16 + t
-            photo_sum = vis_sum;
-            vis_sum = __shfl_down_sync(LFDG_FULL_MASK, vis_sum, 16);
-            neg = __shfl_down_sync(LFDG_FULL_MASK, neg, 16);
-        }
-        const int x_count = kPixBlock * ((n + kPixBlock - 1) / kPixBlock) - neg;
-        // y_nonempty of target t: any occluded pixel among the 16 compute lanes of half t & 1
-        unsigned ym = 0;
-        for (int k = 0; k < (nr + 1) / 2; ++k) {
-            const unsigned m = __ballot_sync(LFDG_FULL_MASK, (occbits >> k) & 1u);
-            if ((lane >> 1) == k) ym = m;
-        }
-        const bool y_nonempty = ((lane & 1) ? (ym >> 16) : (ym & 0xFFFFu)) != 0;
-        if (lane < nr) {
+        if (act) {
             const double photo = photo_sum / (double)n;
             const double vis = x_count > 0 ? photo * (vis_sum / x_count) : 0.0;
-            double occ = 0.0;
-            if (a.use_o && y_nonempty) occ = a.eta * (1.0 - (double)a.min_nb_sim[(size_t)v * a.nsp + sp]);
-            w.res[t0 + lane] = vis + occ;
+            res[t] = vis + (y_nonempty ? occ : 0.0);
         }
     }
     __syncwarp();
     double acc = 0;
-    for (int t = 0; t < N; ++t) acc += w.res[t];
+    for (int t = 0; t < N; ++t) acc += res[t];
     __syncwarp();
     return acc / (double)N;
 }
 
-// The reference's sequential greedy over cand[0, n) (refine.hpp:279-303), candidate by
-// candidate in index order with the running prune E_s (1 + eta) <= e_cur: the same
-// candidates are evaluated as in the reference.  init: cand[0] is the current plane and its
-// energy initialises e_cur (refine.hpp:277).
+// The reference's sequential greedy over cand[base, base + n) (refine.hpp:279-303) with the
+// running prune E_s (1 + eta) <= e_cur.  Candidates are evaluated two at a time when N <= 16 (one
+// per half-warp): the second one speculatively, against the running best before the first is
+// decided.  Decisions are still taken in index order with exact energies — after accepting the
+// first, the second is re-tested against the new best and dropped if the prune now rejects it (it
+// can then not be accepted either) — so the accepted planes and the count are the reference's.
+// init: cand[0] is the current plane and its energy initialises e_cur (refine.hpp:277).
 template <bool kIdR, bool kCanonK, int kFlat>
 __device__ __forceinline__ void greedy(const RefineArgs& a, const WarpSmem& w, int base, int n, int v, int sp, int m0,
                                        int n_members, bool init, double& e_cur, double4& current, unsigned& accepted,
                                        unsigned long long& pix_evals, unsigned& cand_evals) {
     const int lane = threadIdx.x & 31;
     const bool prune = a.use_s && a.use_c;
+    const bool pairs = a.N <= 16 && !init;
     int next = base;
     n += base;
+    // The reference prunes with E_s (1 + eta) <= e_cur (refine.hpp:297).  Here the task's own bound
+    // m_task = 1 + eta (1 - min_nb_sim) >= every V_t + O_t (photo, visibility ratio <= 1, O_t =
+    // eta (1 - min_nb_sim) or 0), padded by 2^-30 against rounding, also prunes: a candidate with
+    // E_s m_task <= e_cur has E <= e_cur and is never accepted, so the winner and the accepted
+    // count are the reference's; only non-accepted evaluations are skipped.  es = -inf marks a
+    // repeat of an earlier plane of this task (mark_repeats).
+    auto passes = [&](int idx) {
+        return w.es[idx] != -INFINITY && (init || !prune || w.es[idx] * w.m_task > e_cur);
+    };
     while (next < n) {
-        // next candidate that survives the prune test (ordered ballot scan)
         const int idx = next + lane;
-        // The reference prunes with E_s (1 + eta) <= e_cur (refine.hpp:297).  Here the task's own
-        // bound m_task = 1 + eta (1 - min_nb_sim) >= every V_t + O_t (photo, visibility ratio <= 1,
-        // O_t = eta (1 - min_nb_sim) or 0), padded by 2^-30 against rounding, also prunes: a
-        // candidate with E_s m_task <= e_cur has E <= e_cur and is never accepted, so the winner
-        // and the accepted count are the reference's; only non-accepted evaluations are skipped.
-        // es = -inf marks a repeat of an earlier plane of this task (mark_repeats).
-        const bool pass = idx < n && w.es[idx] != -INFINITY && (init || !prune || w.es[idx] * w.m_task > e_cur);
-        const unsigned m = __ballot_sync(LFDG_FULL_MASK, pass);
+        const unsigned m = __ballot_sync(LFDG_FULL_MASK, idx < n && passes(idx));
         if (!m) {
             next += 32;
             continue;
         }
-        const int c = next + __ffs(m) - 1;
-        next = c + 1;
-        const double4 cand = w.cand[c];
-        double e;
+        const int c1 = next + __ffs(m) - 1;
+        const unsigned m2 = m & (m - 1);
+        const int c2 = pairs && m2 ? next + __ffs(m2) - 1 : -1;
+        next = (c2 >= 0 ? c2 : c1) + 1;
+        const double4 p1 = w.cand[c1];
+        const double4 p2 = c2 >= 0 ? w.cand[c2] : p1;
+        double e1, e2 = 0;
         if (a.use_c) {
-            const double ec = consistency_warp<kIdR, kCanonK, kFlat>(a, w, v, sp, cand, m0, n_members);
-            e = prune ? w.es[c] * ec : (a.use_s ? 1.0 * w.es[c] : 1.0) * ec;
-            pix_evals += (unsigned long long)a.N * n_members;
+            const double ec = consistency_pair<kIdR, kCanonK, kFlat>(a, w, v, sp, lane < 16 || !pairs ? p1 : p2, m0,
+                                                                     n_members);
+            const double ec1 = __shfl_sync(LFDG_FULL_MASK, ec, 0);
+            const double ec2 = __shfl_sync(LFDG_FULL_MASK, ec, 16);
+            e1 = prune ? w.es[c1] * ec1 : (a.use_s ? 1.0 * w.es[c1] : 1.0) * ec1;
+            if (c2 >= 0) e2 = prune ? w.es[c2] * ec2 : (a.use_s ? 1.0 * w.es[c2] : 1.0) * ec2;
+            pix_evals += (unsigned long long)a.N * n_members * (c2 >= 0 ? 2 : 1);
         } else {
-            e = a.use_s ? 1.0 * w.es[c] : 1.0;
+            e1 = a.use_s ? 1.0 * w.es[c1] : 1.0;
+            if (c2 >= 0) e2 = a.use_s ? 1.0 * w.es[c2] : 1.0;
         }
-        cand_evals++;
+        cand_evals += c2 >= 0 ? 2 : 1;
         if (init) {
-            e_cur = e;
-        } else if (e > e_cur) {
-            e_cur = e;
-            current = cand;
+            e_cur = e1;
+            continue;
+        }
+        if (e1 > e_cur) {
+            e_cur = e1;
+            current = p1;
+            accepted++;
+        }
+        if (c2 >= 0 && passes(c2) && e2 > e_cur) {
+            e_cur = e2;
+            current = p2;
             accepted++;
         }
     }
@@ -535,11 +480,11 @@ __global__ void __launch_bounds__(128, LFDG_REFINE_MIN_BLOCKS) k_refine(RefineAr
     const int gwarp = blockIdx.x * 4 + warp;
     unsigned char* base = smem_raw + warp * warp_smem_bytes(a.N, kFlat);
     WarpSmem w;
-    w.pitch = tile_pitch(a.N);
+    w.cw = cache_width(a.N);
     w.pc = reinterpret_cast<double2*>(base);
-    w.tg = base + (size_t)a.N * kWays * sizeof(double2);
-    w.tile = reinterpret_cast<double2*>(base + (size_t)a.N * kWays * sizeof(double2) + (size_t)a.N * target_row_bytes(kFlat));
-    w.res = reinterpret_cast<double*>(w.tile + kPixBlock * w.pitch);
+    w.tg = base + (size_t)kWays * w.cw * sizeof(double2);
+    w.geo = reinterpret_cast<PixGeo*>(static_cast<unsigned char*>(w.tg) + (size_t)a.N * target_row_bytes(kFlat));
+    w.res = reinterpret_cast<double*>(w.geo + 32);
     w.cand = g_cand + (size_t)gwarp * cap;
     w.es = g_es + (size_t)gwarp * cap;
 
@@ -589,7 +534,7 @@ __global__ void __launch_bounds__(128, LFDG_REFINE_MIN_BLOCKS) k_refine(RefineAr
                 g.ras = a.ras + (size_t)t * a.W * a.H;
             }
         }
-        for (int k = lane; k < a.N * kWays; k += 32)  // new reference colour: empty photo cache
+        for (int k = lane; k < kWays * w.cw; k += 32)  // new reference colour: empty photo cache
             w.pc[k] = make_double2(0.0, __hiloint2double(-1, -1));
         __syncwarp();
 
