@@ -26,7 +26,7 @@ namespace lfdg {
 namespace libm {
 
 #if defined(__CUDACC__)
-__device__ const uint64_t kExpTabDev[256] = LFDG_EXP_TAB_INIT;
+__device__ const __align__(16) uint64_t kExpTabDev[256] = LFDG_EXP_TAB_INIT;
 __device__ const uint64_t kExpfTabDev[32] = LFDG_EXPF_TAB_INIT;
 #endif
 static const uint64_t kExpTabHost[256] = LFDG_EXP_TAB_INIT;
@@ -177,8 +177,14 @@ LFDG_HD double exp_nonpos(double x) {
     kd = kd - LFDG_EXPC(1);
     const double r = fma_(kd, LFDG_EXPC(3), fma_(kd, LFDG_EXPC(2), x));
     const unsigned idx = 2u * (unsigned)(ki & 127u);
+#if defined(__CUDA_ARCH__)
+    const ulonglong2 te = __ldg(reinterpret_cast<const ulonglong2*>(&kExpTabDev[idx]));  // (tail, sbits) pair
+    const double tail = as_f64(te.x);
+    uint64_t sbits = te.y + (ki << 45);
+#else
     const double tail = as_f64(exp_tab(idx));
     uint64_t sbits = exp_tab(idx + 1) + (ki << 45);
+#endif
     const double r2 = r * r;
     const double tmp = fma_(r2 * r2, fma_(r, LFDG_EXPC(7), LFDG_EXPC(6)), fma_(fma_(r, LFDG_EXPC(5), LFDG_EXPC(4)), r2, r + tail));
     if (x <= -512.0) {  // specialcase, k < 0 (abstop == 0 for 512 <= |x| < 1024)

@@ -364,9 +364,10 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
 // first, the second is re-tested against the new best and dropped if the prune now rejects it (it
 // can then not be accepted either) — so the accepted planes and the count are the reference's.
 // init: cand[0] is the current plane and its energy initialises e_cur (refine.hpp:277).
+// current: index in cand of the running plane.
 template <bool kIdR, bool kCanonK, int kFlat>
 __device__ __forceinline__ void greedy(const RefineArgs& a, const WarpSmem& w, int base, int n, int v, int sp, int m0,
-                                       int n_members, bool init, double& e_cur, double4& current, unsigned& accepted,
+                                       int n_members, bool init, double& e_cur, int& current, unsigned& accepted,
                                        unsigned long long& pix_evals, unsigned& cand_evals) {
     const int lane = threadIdx.x & 31;
     const bool prune = a.use_s && a.use_c;
@@ -393,12 +394,10 @@ __device__ __forceinline__ void greedy(const RefineArgs& a, const WarpSmem& w, i
         const unsigned m2 = m & (m - 1);
         const int c2 = pairs && m2 ? next + __ffs(m2) - 1 : -1;
         next = (c2 >= 0 ? c2 : c1) + 1;
-        const double4 p1 = w.cand[c1];
-        const double4 p2 = c2 >= 0 ? w.cand[c2] : p1;
         double e1, e2 = 0;
         if (a.use_c) {
-            const double ec = consistency_pair<kIdR, kCanonK, kFlat>(a, w, v, sp, lane < 16 || !pairs ? p1 : p2, m0,
-                                                                     n_members);
+            const double ec = consistency_pair<kIdR, kCanonK, kFlat>(
+                a, w, v, sp, w.cand[lane < 16 || c2 < 0 ? c1 : c2], m0, n_members);
             const double ec1 = __shfl_sync(LFDG_FULL_MASK, ec, 0);
             const double ec2 = __shfl_sync(LFDG_FULL_MASK, ec, 16);
             e1 = prune ? w.es[c1] * ec1 : (a.use_s ? 1.0 * w.es[c1] : 1.0) * ec1;
@@ -415,12 +414,12 @@ __device__ __forceinline__ void greedy(const RefineArgs& a, const WarpSmem& w, i
         }
         if (e1 > e_cur) {
             e_cur = e1;
-            current = p1;
+            current = c1;
             accepted++;
         }
         if (c2 >= 0 && passes(c2) && e2 > e_cur) {
             e_cur = e2;
-            current = p2;
+            current = c2;
             accepted++;
         }
     }
@@ -509,7 +508,7 @@ __global__ void __launch_bounds__(128, LFDG_REFINE_MIN_BLOCKS) k_refine(RefineAr
         const double4 cur0 = a.planes[vs + sp];
         const int m0 = a.moff[(size_t)v * (a.nsp + 1) + sp];
         const int n_members = a.moff[(size_t)v * (a.nsp + 1) + sp + 1] - m0;
-        double4 current = cur0;
+        int current = 0;  // index in w.cand of the running plane (cand[0] = cur0)
         double e_cur = 0;
         unsigned accepted = 0;
         w.m_task = (a.use_o ? 1.0 + a.eta * (1.0 - (double)a.min_nb_sim[vs + sp]) : 1.0) * (1.0 + 0x1p-30);
@@ -597,7 +596,7 @@ __global__ void __launch_bounds__(128, LFDG_REFINE_MIN_BLOCKS) k_refine(RefineAr
         {
             bool okn = false;
             double4 nc = make_double4(0, 0, 0, 0);
-            const double cur_depth = current.x;
+            const double cur_depth = w.cand[current].x;
             if (lane < 8) {
                 const int k = lane;
                 const int ax_ = gx + kDir[k][0], ay_ = gy + kDir[k][1];
@@ -639,7 +638,7 @@ __global__ void __launch_bounds__(128, LFDG_REFINE_MIN_BLOCKS) k_refine(RefineAr
             greedy<kIdR, kCanonK, kFlat>(a, w, 1 + n_cand, nn, v, sp, m0, n_members, false, e_cur, current, accepted,
                                          pix_evals, cand_evals);
         }
-        if (lane == 0) a.out[vs + sp] = current;
+        if (lane == 0) a.out[vs + sp] = w.cand[current];
         accepted_total += accepted;
         __syncwarp();
     }
