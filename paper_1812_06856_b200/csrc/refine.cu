@@ -168,7 +168,8 @@ struct WarpSmem {
     double* es;     // [cap]   (global scratch)
     void* tg;       // [N] TargetRow, or TargetFlat for kFlat
     PixGeo* geo;    // [32] geometry of the current pixel chunk (one entry per lane)
-    double2* pc;    // [kWays][cw] lane-private photo-weight cache: (weight, raster word)
+    double2* pc;    // [cw][kWays + 1] lane-private photo-weight cache rows: (weight, raster word); the
+                    // pad entry staggers the rows over the banks
     double* res;    // [2][N] V + O per target, per candidate slot
     double m_task;  // upper bound of V_t + O_t for the current task
     int cw;         // photo-cache row width: max(32, N)
@@ -179,7 +180,7 @@ constexpr int kWays = 4;  // photo-cache slots per (lane, target)
 __host__ __device__ inline int cache_width(int N) { return N > 32 ? N : 32; }
 __host__ __device__ inline size_t target_row_bytes(bool flat) { return flat ? sizeof(TargetFlat) : sizeof(TargetRow); }
 __host__ __device__ inline size_t warp_smem_bytes(int N, bool flat) {
-    const size_t b = (size_t)kWays * cache_width(N) * sizeof(double2) + (size_t)N * target_row_bytes(flat) +
+    const size_t b = (size_t)(kWays + 1) * cache_width(N) * sizeof(double2) + (size_t)N * target_row_bytes(flat) +
                      32 * sizeof(PixGeo) + 2 * (size_t)N * sizeof(double);
     return (b + 127) & ~(size_t)127;
 }
@@ -257,7 +258,7 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
     for (int t0 = 0; t0 < N; t0 += G) {
         const int t = t0 + tl;
         const bool act = t < N;
-        const int cslot = G == 16 ? lane : (act ? t : 0);  // this lane's photo-cache column
+        double2* const pcl = w.pc + (G == 16 ? lane : (act ? t : 0)) * (kWays + 1);  // this lane's cache row
         double T0 = 0, T1 = 0;
         const int4* ras = nullptr;
         if (kFlat && act) {
@@ -276,8 +277,9 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
             __syncwarp();
             const int cnt = min(G, n - b);
             if (act) {
-                for (int jj = 0; jj < cnt; ++jj) {
-                    const PixGeo& q = geo[jj];
+                const PixGeo* qp = geo;  // walked as a pointer: a loop-carried register, never recomputed
+                for (int jj = 0; jj < cnt; ++jj, ++qp) {
+                    const PixGeo& q = *qp;
                     if (!q.ok) continue;
                     int px, py;
                     double zt, inv_z;
@@ -319,7 +321,7 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
                     const int4 r = __ldg(ras + (unsigned)(py * a.W + px));
                     if (r.x != cached_word) {  // refine.hpp:147-150
                         const int way = (((unsigned)r.x >> 28) + 2 * ((unsigned)r.x >> 30)) & (kWays - 1);
-                        double2* e = &w.pc[way * w.cw + cslot];
+                        double2* e = pcl + way;
                         const double2 c = *e;
                         if (__double2loint(c.y) == r.x) {
                             cached_w = c.x;
@@ -481,7 +483,7 @@ __global__ void __launch_bounds__(128, LFDG_REFINE_MIN_BLOCKS) k_refine(RefineAr
     WarpSmem w;
     w.cw = cache_width(a.N);
     w.pc = reinterpret_cast<double2*>(base);
-    w.tg = base + (size_t)kWays * w.cw * sizeof(double2);
+    w.tg = base + (size_t)(kWays + 1) * w.cw * sizeof(double2);
     w.geo = reinterpret_cast<PixGeo*>(static_cast<unsigned char*>(w.tg) + (size_t)a.N * target_row_bytes(kFlat));
     w.res = reinterpret_cast<double*>(w.geo + 32);
     w.cand = g_cand + (size_t)gwarp * cap;
@@ -533,7 +535,7 @@ __global__ void __launch_bounds__(128, LFDG_REFINE_MIN_BLOCKS) k_refine(RefineAr
                 g.ras = a.ras + (size_t)t * a.W * a.H;
             }
         }
-        for (int k = lane; k < kWays * w.cw; k += 32)  // new reference colour: empty photo cache
+        for (int k = lane; k < (kWays + 1) * w.cw; k += 32)  // new reference colour: empty photo cache
             w.pc[k] = make_double2(0.0, __hiloint2double(-1, -1));
         __syncwarp();
 
