@@ -276,49 +276,87 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
             w.geo[lane] = pixel_geo<kFlat>(a, mr, b + tl, n, p, plane_num);
             __syncwarp();
             const int cnt = min(G, n - b);
-            if (act) {
+            if (act && kFlat) {
+                // Software-pipelined by one pixel: the raster record of pixel jj + 1 is requested
+                // before pixel jj is consumed, so the gather's latency overlaps the exp.
+                auto issue = [&](const PixGeo* qq, int4& rr) -> bool {
+                    if (!qq->ok) return false;
+                    int px, py;
+                    const double hx = a.uK00 * (qq->sv0 + T0) + qq->f_kz0;
+                    if (!fast_lround(hx * qq->f_inv, px)) px = lround_div(hx, qq->sv2);
+                    if (kFlat == 2) {
+                        py = qq->f_py;
+                    } else {
+                        const double hy = a.uK11 * (qq->sv1 + T1) + qq->f_kz1;
+                        if (!fast_lround(hy * qq->f_inv, py)) py = lround_div(hy, qq->sv2);
+                    }
+                    if ((unsigned)px >= (unsigned)a.W || (unsigned)py >= (unsigned)a.H) return false;
+                    // tgrid.label(px, py) and snapshot.depth[t](px, py) (refine.hpp:146-152) in one
+                    // 16-byte gather: (label word, depth, 1 / (double)depth)
+                    rr = __ldg(ras + (unsigned)(py * a.W + px));
+                    return true;
+                };
+                const PixGeo* qp = geo;  // walked as a pointer: a loop-carried register, never recomputed
+                int4 rn = make_int4(0, 0, 0, 0);
+                bool vn = issue(qp, rn);
+                for (int jj = 0; jj < cnt; ++jj) {
+                    const int4 r = rn;
+                    const bool valid = vn;
+                    const PixGeo* qc = qp++;
+                    if (jj + 1 < cnt) vn = issue(qp, rn);
+                    if (!valid) continue;
+                    const double zt = qc->sv2, inv_z = qc->f_inv;
+                    if (r.x != cached_word) {  // refine.hpp:147-150
+                        const int way = (((unsigned)r.x >> 28) + 2 * ((unsigned)r.x >> 30)) & (kWays - 1);
+                        double2* e = pcl + way;
+                        const double2 c = *e;
+                        if (__double2loint(c.y) == r.x) {
+                            cached_w = c.x;
+                        } else {
+                            cached_w = photo_miss(a.targets + (size_t)v * N + t, a.color + (size_t)v * a.nsp + sp,
+                                                  a.color, a.nsp, r.x & 0x0FFFFFFF, a.inv_two_alpha2);
+                            *e = make_double2(cached_w, __hiloint2double(-1, r.x));
+                        }
+                        cached_word = r.x;
+                    }
+                    photo_sum += cached_w;
+                    const float td = __int_as_float(r.y);
+                    if (td <= 0) continue;  // no target depth: not in X or Y
+                    if (zt <= (double)td * (1.0 + 1e-6)) {
+                        const double rr = inv_z - __hiloint2double(r.w, r.z);
+                        vis_sum += libm::exp_nonpos(-rr * rr * a.inv_two_sigma2);
+                        ++x_count;
+                    } else {
+                        y_nonempty = true;
+                    }
+                }
+            } else if (act) {
                 const PixGeo* qp = geo;  // walked as a pointer: a loop-carried register, never recomputed
                 for (int jj = 0; jj < cnt; ++jj, ++qp) {
                     const PixGeo& q = *qp;
                     if (!q.ok) continue;
                     int px, py;
                     double zt, inv_z;
-                    if (kFlat) {
-                        const double hx = a.uK00 * (q.sv0 + T0) + q.f_kz0;
-                        if (!fast_lround(hx * q.f_inv, px)) px = lround_div(hx, q.sv2);
-                        if (kFlat == 2) {
-                            py = q.f_py;
-                        } else {
-                            const double hy = a.uK11 * (q.sv1 + T1) + q.f_kz1;
-                            if (!fast_lround(hy * q.f_inv, py)) py = lround_div(hy, q.sv2);
-                        }
-                        zt = q.sv2;
-                        inv_z = q.f_inv;
+                    const TargetRow& g = static_cast<const TargetRow*>(w.tg)[t];
+                    double x0, x1, x2;
+                    if (kIdR) {
+                        x0 = q.sv0 + g.T[0];
+                        x1 = q.sv1 + g.T[1];
+                        x2 = q.sv2 + g.T[2];
                     } else {
-                        const TargetRow& g = static_cast<const TargetRow*>(w.tg)[t];
-                        double x0, x1, x2;
-                        if (kIdR) {
-                            x0 = q.sv0 + g.T[0];
-                            x1 = q.sv1 + g.T[1];
-                            x2 = q.sv2 + g.T[2];
-                        } else {
-                            x0 = ((g.R[0] * q.sv0 + g.R[1] * q.sv1) + g.R[2] * q.sv2) + g.T[0];
-                            x1 = ((g.R[3] * q.sv0 + g.R[4] * q.sv1) + g.R[5] * q.sv2) + g.T[1];
-                            x2 = ((g.R[6] * q.sv0 + g.R[7] * q.sv1) + g.R[8] * q.sv2) + g.T[2];
-                        }
-                        if (!(x2 > 0)) continue;  // behind the target camera
-                        const double hx = kCanonK ? g.K00 * x0 + g.K02 * x2 : (g.K00 * x0 + g.K01 * x1) + g.K02 * x2;
-                        const double hy = g.K11 * x1 + g.K12 * x2;
-                        inv_z = 1.0 / x2;
-                        if (!fast_lround(hx * inv_z, px)) px = lround_div(hx, x2);
-                        if (!fast_lround(hy * inv_z, py)) py = lround_div(hy, x2);
-                        zt = x2;
-                        ras = g.ras;
+                        x0 = ((g.R[0] * q.sv0 + g.R[1] * q.sv1) + g.R[2] * q.sv2) + g.T[0];
+                        x1 = ((g.R[3] * q.sv0 + g.R[4] * q.sv1) + g.R[5] * q.sv2) + g.T[1];
+                        x2 = ((g.R[6] * q.sv0 + g.R[7] * q.sv1) + g.R[8] * q.sv2) + g.T[2];
                     }
+                    if (!(x2 > 0)) continue;  // behind the target camera
+                    const double hx = kCanonK ? g.K00 * x0 + g.K02 * x2 : (g.K00 * x0 + g.K01 * x1) + g.K02 * x2;
+                    const double hy = g.K11 * x1 + g.K12 * x2;
+                    inv_z = 1.0 / x2;
+                    if (!fast_lround(hx * inv_z, px)) px = lround_div(hx, x2);
+                    if (!fast_lround(hy * inv_z, py)) py = lround_div(hy, x2);
+                    zt = x2;
                     if ((unsigned)px >= (unsigned)a.W || (unsigned)py >= (unsigned)a.H) continue;
-                    // tgrid.label(px, py) and snapshot.depth[t](px, py) (refine.hpp:146-152) in one
-                    // 16-byte gather: (label word, depth, 1 / (double)depth)
-                    const int4 r = __ldg(ras + (unsigned)(py * a.W + px));
+                    const int4 r = __ldg(g.ras + (unsigned)(py * a.W + px));
                     if (r.x != cached_word) {  // refine.hpp:147-150
                         const int way = (((unsigned)r.x >> 28) + 2 * ((unsigned)r.x >> 30)) & (kWays - 1);
                         double2* e = pcl + way;
