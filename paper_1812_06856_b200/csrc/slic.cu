@@ -70,6 +70,10 @@ __global__ void __launch_bounds__(128) k_slic_assign(const float4* __restrict__ 
     const float4* ccb = ccol + (size_t)b * nsp;
     const int pgx = x / S, pgy = y / S;
     const float two_s = 2.f * S;
+    // ds = (float)sqrt(D) > 2S is decided on D alone outside a +-2^-20 band around (2S)^2: there
+    // the float rounding of the square root cannot move ds across 2S (ulp(2S) <= 2^-23 2S), so
+    // the double square root is only taken for candidates that can be in range.
+    const double d_far = (double)two_s * two_s * (1.0 + 0x1p-20);
     float best_d = 0.f, best_s = 0.f;
     int best = -1;
     const int gy0 = max(0, pgy - 2), gy1 = min(gh - 1, pgy + 2);
@@ -79,7 +83,9 @@ __global__ void __launch_bounds__(128) k_slic_assign(const float4* __restrict__ 
             const int id = gy * gw + gx;
             const double ddx = (double)x - cxb[id];
             const double ddy = (double)y - cyb[id];
-            const float ds = (float)sqrt(ddx * ddx + ddy * ddy);
+            const double D = ddx * ddx + ddy * ddy;
+            if (D > d_far) continue;  // ds > 2S for sure
+            const float ds = (float)sqrt(D);
             if (ds > two_s) continue;
             const float4 c = ccb[id];
             const float dc = sqrtf(color_dist2(pc.x, pc.y, pc.z, c.x, c.y, c.z));
