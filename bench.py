@@ -154,7 +154,7 @@ def reference_sample(st: dict, step: int, workers: int) -> dict:
     t = time.time()
     s.slic(view, c["S"], 0.1, 10, workers)
     t_slic = time.time() - t
-    n_sw = max(64, 48 * workers)
+    n_sw = min(nsp, max(64, 48 * workers))
     sps = rng.choice(nsp, n_sw, replace=False)
     t = time.time()
     s.sweep_sample(view, sps, c["levels"], 0.05, c["max_neighbors"], 0, workers)
