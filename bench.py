@@ -241,7 +241,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     torch.cuda.set_device(dev)
     c = scenes.CONFIGS[args.config]
     threads = max(1, cpu_cores() // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world))))
-    sc = scenes.render_config(args.config, threads=threads, gt=False)
+    sc = scenes.render_config(args.config, threads=threads, gt=False, rgb=not args.no_e2e)
     V = sc["lab"].shape[0]
     cfg = HotPathConfig(SlicParams(c["S"], 0.1, 10), SweepParams(c["levels"], 0.05, c["max_neighbors"]),
                         EnergyParams(iterations=c["iterations"], max_neighbors=c["max_neighbors"]), seed=0)
@@ -325,6 +325,22 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                "h2d_bytes_per_step": int(host_imgs.nbytes),
                "d2h_bytes_per_step": int(planes_pin.nbytes + depth_pin.nbytes) * world,
                "ms_per_step": float(te[0]) / args.steps}
+        # the same from sRGB host images: rgb_to_scaled_lab runs on the GPU (lfdg_upload_rgb) instead
+        # of the reference's host pre-pass (pipeline.hpp:245)
+        host_imgs[...] = sc["rgb"]
+        barrier()
+        f0.record(stream)
+        for _ in range(args.steps):
+            hp.upload_rgb(host_imgs)
+            hp.run()
+            hp.download(planes_pin, depth_pin, sync=False)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([f0.elapsed_time(f1)], device=f"cuda:{dev}", dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e["from_srgb"] = {"value": V * args.steps / (float(te[0]) / 1e3), "unit": UNIT,
+                            "h2d_bytes_per_step": int(host_imgs.nbytes), "ms_per_step": float(te[0]) / args.steps}
 
     if rank != 0:
         return

@@ -144,6 +144,10 @@ int lfdg_set_depth(lfdg_ctx* ctx, int view, const float* depth);
 /* Enqueue the upload of views [v0, v0+n) from host [n][H][W][3] scaled-LAB floats (pinned memory
  * makes it one async DMA); the images replace the context's copies. */
 int lfdg_upload_images(lfdg_ctx* ctx, int v0, int n, const float* images);
+/* Enqueue the upload of views [v0, v0+n) from host [n][H][W][3] sRGB floats in [0, 1] and their
+ * conversion to scaled LAB on the device: rgb_to_scaled_lab (image.hpp:97-107), bit-identical to
+ * the reference (glibc powf / cbrtf ports), replacing the host pre-pass of pipeline.hpp:245. */
+int lfdg_upload_rgb(lfdg_ctx* ctx, int v0, int n, const float* rgb);
 /* Enqueue the download of planes [n][nsp] and depth [n][H][W] of views [v0, v0+n) (either may be
  * NULL); sync != 0 waits for completion. */
 int lfdg_download_results(lfdg_ctx* ctx, int v0, int n, lfdg_plane* planes, float* depth, int sync);
@@ -203,6 +207,8 @@ int lfdg_render_scene(int kind, int n_views, int width, int height, double f, do
                       lfdg_camera* cams_out, double* range_out);
 /* rgb_to_scaled_lab (image.hpp:83-107) over n pixels of [n][3] floats. */
 int lfdg_rgb_to_scaled_lab(int64_t n_pixels, const float* rgb, float* lab);
+/* rgb_to_scaled_lab (image.hpp:97-107) on the GPU for n host pixels ([n][3] in, [n][3] out). */
+int lfdg_rgb_to_scaled_lab_gpu(int device, const float* rgb, float* lab, size_t n);
 
 /* ---- self-test ------------------------------------------------------------------------- */
 /* Device ports of glibc exp / expf used by the energy (glibc_math.cuh), on caller inputs. */

@@ -65,7 +65,8 @@ EXPORTED = [
     "lfdg_run_refinement", "lfdg_get_min_nb_sim", "lfdg_device_buffer", "lfdg_mark_views_ready",
     "lfdg_selftest_exp", "lfdg_selftest_expf", "lfdg_render_scene", "lfdg_rgb_to_scaled_lab",
     "lfdg_upload_images", "lfdg_download_results", "lfdg_selftest_fp64_peak", "lfdg_refine_work", "lfdg_selftest_exp_nonpos",
-    "lfdg_fuse_views", "lfdg_get_fused", "lfdg_gather_candidates", "lfdg_stability_fuse",
+    "lfdg_fuse_views", "lfdg_get_fused", "lfdg_gather_candidates", "lfdg_stability_fuse", "lfdg_upload_rgb",
+    "lfdg_rgb_to_scaled_lab_gpu",
 ]
 
 _lib = None
@@ -142,6 +143,8 @@ def lib():
         "lfdg_render_scene": (I, [I, I, I, I, D, D, D, I, I, I, P, P, P, P, P]),
         "lfdg_rgb_to_scaled_lab": (I, [C.c_int64, P, P]),
         "lfdg_upload_images": (I, [P, I, I, P]),
+        "lfdg_upload_rgb": (I, [P, I, I, P]),
+        "lfdg_rgb_to_scaled_lab_gpu": (I, [I, P, P, C.c_size_t]),
         "lfdg_download_results": (I, [P, I, I, P, P, I]),
         "lfdg_selftest_fp64_peak": (I, [I, C.POINTER(D)]),
         "lfdg_refine_work": (I, [P, PU64, PU64, I]),

@@ -172,6 +172,13 @@ class DeviceContext:
     def synchronize(self):
         N.check(self.L.lfdg_synchronize(self.h))
 
+    def upload_rgb(self, rgb: np.ndarray, v0: int = 0):
+        """Replace the LAB images of views [v0, v0 + n) by rgb_to_scaled_lab (image.hpp:97-107) of the
+        sRGB images rgb [n][H][W][3], converted on the device (bit-identical to the reference)."""
+        rgb = np.ascontiguousarray(rgb, np.float32)
+        N.check(self.L.lfdg_upload_rgb(self.h, v0, rgb.shape[0], N.ptr(rgb)))
+        self.synchronize()
+
     def launch_count(self) -> int:
         return int(self.L.lfdg_launch_count(self.h))
 
@@ -457,3 +464,11 @@ def run_refinement(rctx: RefineContext, state: PlaneMap, workers: int = 1,
         state = refine_iteration(rctx, state, l, stats=stats)
         rasterize(rctx.mvs, rctx.grids, state)
     return state
+
+
+def rgb_to_scaled_lab(rgb: np.ndarray, device: int = 0) -> np.ndarray:
+    """rgb_to_scaled_lab (image.hpp:97-107) of an sRGB array [..., 3] on the GPU."""
+    rgb = np.ascontiguousarray(rgb, np.float32)
+    out = np.empty_like(rgb)
+    N.check(N.lib().lfdg_rgb_to_scaled_lab_gpu(device, N.ptr(rgb), N.ptr(out), rgb.size // 3))
+    return out

@@ -242,5 +242,151 @@ LFDG_HD float expf(float x) {
     return (float)y;
 }
 
+// ---- powf / cbrtf for rgb_to_scaled_lab (image.hpp:70-95) -----------------------------------
+// __powf_fma: glibc 2.39 sysdeps/ieee754/flt-32/e_powf.c (the ARM optimized-routines powf) as
+// built for x86-64 with FMA (the IFUNC variant both hosts run).  FMA placement read off
+// `objdump -d libm.so.6` (0x7df50); log2 table (16 x {invc, logc}) and polynomial constants
+// copied from .rodata 0xb7f80 / 0xb8080; exp2 uses __exp2f_data (the expf table above).
+#define LFDG_POWF_LOG2_TAB_INIT                                                                         \
+    {0x1.661ec79f8f3bep+0, -0x1.efec65b963019p-2, 0x1.571ed4aaf883dp+0, -0x1.b0b6832d4fca4p-2,            \
+     0x1.49539f0f010b0p+0, -0x1.7418b0a1fb77bp-2, 0x1.3c995b0b80385p+0, -0x1.39de91a6dcf7bp-2,            \
+     0x1.30d190c8864a5p+0, -0x1.01d9bf3f2b631p-2, 0x1.25e227b0b8ea0p+0, -0x1.97c1d1b3b7af0p-3,            \
+     0x1.1bb4a4a1a343fp+0, -0x1.2f9e393af3c9fp-3, 0x1.12358f08ae5bap+0, -0x1.960cbbf788d5cp-4,            \
+     0x1.0953f419900a7p+0, -0x1.a6f9db6475fcep-5, 0x1.0000000000000p+0, 0x0.0p+0,                         \
+     0x1.e608cfd9a47acp-1, 0x1.338ca9f24f53dp-4,  0x1.ca4b31f026aa0p-1, 0x1.476a9543891bap-3,             \
+     0x1.b2036576afce6p-1, 0x1.e840b4ac4e4d2p-3,  0x1.9c2d163a1aa2dp-1, 0x1.40645f0c6651cp-2,             \
+     0x1.886e6037841edp-1, 0x1.88e9c2c1b9ff8p-2,  0x1.767dcf5534862p-1, 0x1.ce0a44eb17bccp-2}
+#define LFDG_CBRTF_FACTOR_INIT \
+    {0x1.428a2f98d728ap-1, 0x1.965fea53d6e3cp-1, 0x1.0p+0, 0x1.428a2f98d728bp+0, 0x1.965fea53d6e3dp+0}
+#if defined(__CUDACC__)
+__device__ const __align__(16) double kPowfLog2Dev[32] = LFDG_POWF_LOG2_TAB_INIT;  // {invc, logc} x 16
+__device__ const double kCbrtfFactorDev[5] = LFDG_CBRTF_FACTOR_INIT;
+#endif
+static const double kPowfLog2Host[32] = LFDG_POWF_LOG2_TAB_INIT;
+static const double kCbrtfFactorHost[5] = LFDG_CBRTF_FACTOR_INIT;
+LFDG_HD double powf_log2_tab(int i) {  // .rodata 0xb7f80: invc at 2i, logc at 2i + 1
+#if defined(__CUDA_ARCH__)
+    return __ldg(&kPowfLog2Dev[i]);
+#else
+    return kPowfLog2Host[i];
+#endif
+}
+LFDG_HD double cbrtf_factor(int i) {  // .rodata 0xab1c0
+#if defined(__CUDA_ARCH__)
+    return __ldg(&kCbrtfFactorDev[i]);
+#else
+    return kCbrtfFactorHost[i];
+#endif
+}
+
+// powf(x, y) for x > 0 (normal, subnormal, +inf) or NaN, and y finite and nonzero — the only
+// operands rgb_to_scaled_lab produces ((v + 0.055) / 1.055 with v > 0.04045, y = 2.4).
+LFDG_HD float powf_pos(float x, float y) {
+    uint32_t ix = as_u32(x);
+    if (ix >= 0x7f800000u) return x + y;  // +inf -> +inf for y > 0, NaN -> NaN
+    if (ix < 0x00800000u) {               // subnormal x: normalise (e_powf.c)
+        ix = as_u32(x * 0x1p23f) & 0x7fffffffu;
+        ix -= 23u << 23;
+    }
+    // log2_inline
+    const uint32_t tmp = ix - 0x3f330000u;
+    const int i = (int)((tmp >> 19) & 15u);
+    const uint32_t top = tmp & 0xff800000u;
+    const uint32_t iz = ix - top;
+    const int k = (int32_t)top >> 23;
+    union {
+        uint32_t u;
+        float f;
+    } zu;
+    zu.u = iz;
+    const double z = (double)zu.f;
+    const double r = fma_(z, powf_log2_tab(2 * i), -1.0);
+    const double y0 = (double)k + powf_log2_tab(2 * i + 1);
+    double yl = fma_(r, 0x1.27616c9496e0bp-2, -0x1.71969a075c67ap-2);
+    const double p = fma_(r, 0x1.ec70a6ca7baddp-2, -0x1.7154748bef6c8p-1);
+    const double r2 = r * r;
+    double q = fma_(r, 0x1.71547652ab82bp+0, y0);
+    const double r4 = r2 * r2;
+    q = fma_(r2, p, q);
+    yl = fma_(yl, r4, q);
+    const double ylogx = (double)y * yl;
+    if (((as_u64(ylogx) >> 47) & 0xffffu) > 0x80beu) {  // |y log2 x| >= 126
+        if (ylogx > 0x1.fffffffd1d571p+6) return (float)as_f64(0x7ff0000000000000ull);  // __math_oflowf
+        if (ylogx <= -150.0) return 0.0f;                                               // __math_uflowf
+        if (ylogx < -149.0) return 0x1p-149f;  // __math_may_uflowf: 0x1.4p-75f * 0x1.4p-75f
+    }
+    // exp2_inline (sign_bias 0)
+    double kd = ylogx + 0x1.8p+47;
+    const uint64_t ki = as_u64(kd);
+    kd = kd - 0x1.8p+47;
+    const double rr = ylogx - kd;
+    const uint64_t t = expf_tab((unsigned)(ki & 31u)) + (ki << 47);
+    const double sc = as_f64(t);
+    const double zz = fma_(rr, 0x1.c6af84b912394p-5, 0x1.ebfce50fac4f3p-3);
+    const double rr2 = rr * rr;
+    double yy = fma_(rr, 0x1.62e42ff0c52d6p-1, 1.0);
+    yy = fma_(zz, rr2, yy);
+    return (float)(yy * sc);
+}
+
+// cbrtf: glibc 2.39 sysdeps/ieee754/flt-32/s_cbrtf.c (double arithmetic, no FMA; constants and
+// the factor table from .rodata 0x99f40 / 0xab1c0, operation order read off the disassembly).
+LFDG_HD float cbrtf_(float x) {
+    const uint32_t ux = as_u32(x) & 0x7fffffffu;
+    if (ux == 0u || ux >= 0x7f800000u) return x + x;  // zero, inf, NaN
+    // frexpf(|x|)
+    int xe;
+    union {
+        uint32_t u;
+        float f;
+    } m;
+    if (ux < 0x00800000u) {  // subnormal
+        m.u = ux;
+        m.f *= 0x1p25f;
+        xe = (int)(m.u >> 23) - 126 - 25;
+    } else {
+        xe = (int)(ux >> 23) - 126;
+        m.u = ux;
+    }
+    m.u = (m.u & 0x807fffffu) | (126u << 23);
+    const double xm = (double)m.f;
+    const float u = (float)(((0x1.6527f4927f555p-1 - 0x1.8832490c2feddp-3 * xm) * xm) + 0x1.f87bc378ed415p-2);
+    const float t2 = (u * u) * u;
+    const double ud = (double)u, t2d = (double)t2;
+    const double ym = (((xm + xm) + t2d) * ud) / ((t2d + t2d) + xm) * cbrtf_factor(2 + xe % 3);
+    const float r = (float)ym;
+    // ldexpf(+-ym, xe / 3): ym in (0.5, 1.6], the scaled result is a normal float for every
+    // finite x (|cbrt(x)| >= 2^-50)
+    union {
+        uint32_t u;
+        float f;
+    } o;
+    o.f = r;
+    o.u += (uint32_t)(xe / 3) << 23;
+    return (as_u32(x) >> 31) ? -o.f : o.f;
+}
+
+// rgb_to_scaled_lab (image.hpp:70-95), float arithmetic in the reference's order.
+LFDG_HD float srgb_to_linear(float v) { return v <= 0.04045f ? v / 12.92f : powf_pos((v + 0.055f) / 1.055f, 2.4f); }
+LFDG_HD float lab_f(float t) {
+    const float kEps = 216.f / 24389.f;
+    const float kKappa = 24389.f / 27.f;
+    return t > kEps ? cbrtf_(t) : (kKappa * t + 16.f) / 116.f;
+}
+LFDG_HD void rgb_to_scaled_lab(float r0, float g0, float b0, float& L, float& A, float& B) {
+    const float r = srgb_to_linear(r0);
+    const float g = srgb_to_linear(g0);
+    const float b = srgb_to_linear(b0);
+    const float xr = (0.4124564f * r + 0.3575761f * g + 0.1804375f * b) / 0.95047f;
+    const float yr = (0.2126729f * r + 0.7151522f * g + 0.0721750f * b);
+    const float zr = (0.0193339f * r + 0.1191920f * g + 0.9503041f * b) / 1.08883f;
+    const float fx = lab_f(xr);
+    const float fy = lab_f(yr);
+    const float fz = lab_f(zr);
+    L = (116.f * fy - 16.f) / 100.f;
+    A = (500.f * (fx - fy)) / 100.f;
+    B = (200.f * (fy - fz)) / 100.f;
+}
+
 }  // namespace libm
 }  // namespace lfdg

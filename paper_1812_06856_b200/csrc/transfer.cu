@@ -3,6 +3,7 @@
 // buffer and a repack kernel into the float4 layout the kernels gather from, so a pinned
 // source is one DMA per view (no host-side reformatting).
 #include "context.h"
+#include "glibc_math.cuh"
 
 namespace lfdg {
 namespace {
@@ -10,7 +11,31 @@ __global__ void k_repack(const float* __restrict__ src, float4* __restrict__ dst
     const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) dst[i] = make_float4(src[3 * i], src[3 * i + 1], src[3 * i + 2], 0.f);
 }
+// rgb_to_scaled_lab (image.hpp:97-107) fused with the repack: sRGB [n][3] -> scaled LAB float4,
+// bit-identical to the reference through the glibc powf / cbrtf ports (glibc_math.cuh).
+__global__ void k_rgb_to_lab(const float* __restrict__ src, float4* __restrict__ dst, size_t n) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float L, A, B;
+    libm::rgb_to_scaled_lab(src[3 * i], src[3 * i + 1], src[3 * i + 2], L, A, B);
+    dst[i] = make_float4(L, A, B, 0.f);
+}
 }  // namespace
+
+// sRGB images in ([n][H][W][3] floats in [0, 1]), converted to the scaled LAB the hot path reads
+// on the device (the reference converts on the host before the path, pipeline.hpp:245).
+void upload_rgb(Ctx& c, int v0, int n, const float* host) {
+    c.require_views();
+    if (v0 < 0 || n < 0 || v0 + n > c.V) throw Error(LFDG_STATE, "view range out of bounds");
+    if (n == 0) return;
+    const size_t hw = c.hw();
+    StagingScratch& s = c.stage_s;
+    s.buf.alloc((size_t)c.V * hw * 3);
+    LFDG_CUDA_CHECK(cudaMemcpyAsync(s.buf.p, host, (size_t)n * hw * 3 * sizeof(float), cudaMemcpyHostToDevice, c.stream));
+    const size_t m = (size_t)n * hw;
+    k_rgb_to_lab<<<(unsigned)((m + 255) / 256), 256, 0, c.stream>>>(s.buf.p, c.lab.p + (size_t)v0 * hw, m);
+    LFDG_LAUNCHED(&c);
+}
 
 void upload_images(Ctx& c, int v0, int n, const float* host) {
     c.require_views();
@@ -46,6 +71,40 @@ int lfdg_upload_images(lfdg_ctx* p, int v0, int n, const float* images) {
         if (!c) throw lfdg::Error(LFDG_STATE, "null context");
         LFDG_CUDA_CHECK(cudaSetDevice(c->device));
         lfdg::upload_images(*c, v0, n, images);
+        return LFDG_OK;
+    } catch (const lfdg::Error& e) {
+        lfdg::set_last_error(e.what());
+        return e.code;
+    }
+}
+
+int lfdg_upload_rgb(lfdg_ctx* p, int v0, int n, const float* rgb) {
+    try {
+        auto* c = reinterpret_cast<lfdg::Ctx*>(p);
+        if (!c) throw lfdg::Error(LFDG_STATE, "null context");
+        LFDG_CUDA_CHECK(cudaSetDevice(c->device));
+        lfdg::upload_rgb(*c, v0, n, rgb);
+        return LFDG_OK;
+    } catch (const lfdg::Error& e) {
+        lfdg::set_last_error(e.what());
+        return e.code;
+    }
+}
+
+int lfdg_rgb_to_scaled_lab_gpu(int device, const float* rgb, float* lab, size_t n) {
+    try {
+        LFDG_CUDA_CHECK(cudaSetDevice(device));
+        float* din = nullptr;
+        float4* dout = nullptr;
+        LFDG_CUDA_CHECK(cudaMalloc(&din, n * 3 * sizeof(float)));
+        LFDG_CUDA_CHECK(cudaMalloc(&dout, n * sizeof(float4)));
+        LFDG_CUDA_CHECK(cudaMemcpy(din, rgb, n * 3 * sizeof(float), cudaMemcpyHostToDevice));
+        lfdg::k_rgb_to_lab<<<(unsigned)((n + 255) / 256), 256>>>(din, dout, n);
+        LFDG_CUDA_CHECK(cudaGetLastError());
+        LFDG_CUDA_CHECK(cudaMemcpy2D(lab, 3 * sizeof(float), dout, sizeof(float4), 3 * sizeof(float), n,
+                                     cudaMemcpyDeviceToHost));
+        cudaFree(din);
+        cudaFree(dout);
         return LFDG_OK;
     } catch (const lfdg::Error& e) {
         lfdg::set_last_error(e.what());

@@ -142,6 +142,12 @@ class HotPath:
         images_host = np.ascontiguousarray(images_host, np.float32)
         N.check(N.lib().lfdg_upload_images(self.ctx.h, 0, self.V, N.ptr(images_host)))
 
+    def upload_rgb(self, rgb_host: np.ndarray):
+        """Enqueue the H2D copy of every view's sRGB image and its conversion to scaled LAB on the
+        device (rgb_to_scaled_lab, image.hpp:97-107; the reference does it on the host)."""
+        rgb_host = np.ascontiguousarray(rgb_host, np.float32)
+        N.check(N.lib().lfdg_upload_rgb(self.ctx.h, 0, self.V, N.ptr(rgb_host)))
+
     def download(self, planes_host: Optional[np.ndarray], depth_host: Optional[np.ndarray], sync: bool = True):
         """Enqueue the D2H copy of this rank's views' planes [n][nsp][4] and depth [n][H][W]."""
         N.check(N.lib().lfdg_download_results(self.ctx.h, self.v0, self.n,

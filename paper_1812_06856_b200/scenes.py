@@ -39,7 +39,7 @@ def render_scene(kind="cluttered", n_views=3, width=320, height=240, f=320.0, ba
     return dict(lab=lab, rgb=rgb_a, gt=gt_a, cams=cams, range=(float(rng[0]), float(rng[1])))
 
 
-def render_config(name: str, threads: int = 0, gt: bool = True):
+def render_config(name: str, threads: int = 0, gt: bool = True, rgb: bool = False):
     c = CONFIGS[name]
     return render_scene(c["kind"], c["n_views"], c["width"], c["height"], c["f"], c["baseline"], 0.0, c["grid"],
-                        threads=threads, gt=gt)
+                        threads=threads, gt=gt, rgb=rgb)
