@@ -210,6 +210,16 @@ int lfdg_rgb_to_scaled_lab(int64_t n_pixels, const float* rgb, float* lab);
 /* rgb_to_scaled_lab (image.hpp:97-107) on the GPU for n host pixels ([n][3] in, [n][3] out). */
 int lfdg_rgb_to_scaled_lab_gpu(int device, const float* rgb, float* lab, size_t n);
 
+/* ---- evaluation (eval.hpp; the per-view report of run_pipeline, pipeline.hpp:452-466) ------ */
+/* compute_nocc_mask(gt, cams, view, inv_depth_tol) on the ground-truth depths [V][H][W]; both
+ * depth maps to the disparity domain (focal, baseline > 0, + mark_disc) or to inverse depth;
+ * bad_pixel_rate of est_depth [H][W] for every threshold and region: rates[3 t + r] with
+ * r = 0 nocc, 1 all, 2 disc, -1 for an empty region (EmptyRegion).  mask_out [H][W] (NULL
+ * allowed) receives the Region labels (0 Nocc, 1 All, 2 Disc, 3 Ignore).  Host buffers. */
+int lfdg_eval_bad_pixel(int device, int n_views, int width, int height, const float* gt_depth, const lfdg_camera* cams,
+                        int view, const float* est_depth, double inv_depth_tol, double focal, double baseline,
+                        const double* thresholds, int n_thresholds, double* rates, unsigned char* mask_out);
+
 /* ---- self-test ------------------------------------------------------------------------- */
 /* Device ports of glibc exp / expf used by the energy (glibc_math.cuh), on caller inputs. */
 int lfdg_selftest_exp(int device, const double* in, double* out, size_t n);

@@ -66,7 +66,7 @@ EXPORTED = [
     "lfdg_selftest_exp", "lfdg_selftest_expf", "lfdg_render_scene", "lfdg_rgb_to_scaled_lab",
     "lfdg_upload_images", "lfdg_download_results", "lfdg_selftest_fp64_peak", "lfdg_refine_work", "lfdg_selftest_exp_nonpos",
     "lfdg_fuse_views", "lfdg_get_fused", "lfdg_gather_candidates", "lfdg_stability_fuse", "lfdg_upload_rgb",
-    "lfdg_rgb_to_scaled_lab_gpu",
+    "lfdg_rgb_to_scaled_lab_gpu", "lfdg_eval_bad_pixel",
 ]
 
 _lib = None
@@ -144,6 +144,7 @@ def lib():
         "lfdg_rgb_to_scaled_lab": (I, [C.c_int64, P, P]),
         "lfdg_upload_images": (I, [P, I, I, P]),
         "lfdg_upload_rgb": (I, [P, I, I, P]),
+        "lfdg_eval_bad_pixel": (I, [I, I, I, I, P, P, I, P, C.c_double, C.c_double, C.c_double, P, I, P, P]),
         "lfdg_rgb_to_scaled_lab_gpu": (I, [I, P, P, C.c_size_t]),
         "lfdg_download_results": (I, [P, I, I, P, P, I]),
         "lfdg_selftest_fp64_peak": (I, [I, C.POINTER(D)]),

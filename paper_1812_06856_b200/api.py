@@ -472,3 +472,22 @@ def rgb_to_scaled_lab(rgb: np.ndarray, device: int = 0) -> np.ndarray:
     out = np.empty_like(rgb)
     N.check(N.lib().lfdg_rgb_to_scaled_lab_gpu(device, N.ptr(rgb), N.ptr(out), rgb.size // 3))
     return out
+
+
+def eval_bad_pixel(gt_depth: np.ndarray, cams: np.ndarray, view: int, est_depth: np.ndarray, inv_depth_tol: float,
+                   thresholds, focal: float = 0.0, baseline: float = 0.0, device: int = 0, with_mask: bool = False):
+    """run_pipeline's per-view evaluation (pipeline.hpp:452-466; eval.hpp) on the GPU:
+    compute_nocc_mask + (disparity domain: depth_to_disparity + mark_disc | inverse depth) +
+    bad_pixel_rate for each threshold and region.  Returns rates [n_thresholds][3] (nocc, all,
+    disc; -1 = empty region) and optionally the Region mask."""
+    gt = np.ascontiguousarray(gt_depth, np.float32)
+    est = np.ascontiguousarray(est_depth, np.float32)
+    cm = np.ascontiguousarray(cams, np.float64)
+    V, H, W = gt.shape
+    thr = np.ascontiguousarray(thresholds, np.float64)
+    rates = np.zeros((len(thr), 3), np.float64)
+    mask = np.zeros((H, W), np.uint8) if with_mask else None
+    N.check(N.lib().lfdg_eval_bad_pixel(device, V, W, H, N.ptr(gt), N.ptr(cm), view, N.ptr(est), inv_depth_tol, focal,
+                                        baseline, N.ptr(thr), len(thr), N.ptr(rates),
+                                        None if mask is None else N.ptr(mask)))
+    return (rates, mask) if with_mask else rates
