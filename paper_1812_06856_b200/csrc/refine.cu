@@ -177,7 +177,9 @@ struct WarpSmem {
 constexpr int kMaxTargets = 64;
 constexpr int kWays = 4;  // photo-cache slots per (lane, target)
 
-__host__ __device__ inline int cache_width(int N) { return N > 32 ? N : 32; }
+// rows of the photo cache: lane + t0 over the target groups (N <= 32: the 32 lanes; G = 16: one
+// row per (candidate slot, target); G = 32: one per target)
+__host__ __device__ inline int cache_width(int N) { return N > 32 ? (N + 31) / 32 * 32 : 32; }
 __host__ __device__ inline size_t target_row_bytes(bool flat) { return flat ? sizeof(TargetFlat) : sizeof(TargetRow); }
 __host__ __device__ inline size_t warp_smem_bytes(int N, bool flat) {
     const size_t b = (size_t)(kWays + 1) * cache_width(N) * sizeof(double2) + (size_t)N * target_row_bytes(flat) +
@@ -258,7 +260,7 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
     for (int t0 = 0; t0 < N; t0 += G) {
         const int t = t0 + tl;
         const bool act = t < N;
-        double2* const pcl = w.pc + (G == 16 ? lane : (act ? t : 0)) * (kWays + 1);  // this lane's cache row
+        double2* const pcl = w.pc + (lane + t0) * (kWays + 1);  // this lane's cache row
         double T0 = 0, T1 = 0;
         const int4* ras = nullptr;
         if (kFlat && act) {
