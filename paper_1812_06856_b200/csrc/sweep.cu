@@ -24,6 +24,70 @@ namespace {
 
 constexpr int kSweepCap = 1024;  // member pixels staged per chunk
 
+// Packed f32x2 arithmetic (two colour channels per instruction).  Products go through
+// fma.rn.f32x2(a, b, +0.0) and are added by a separate add.rn.f32x2: ptxas does not fuse that
+// pair (it does fuse a plain mul.rn.f32x2 + add.rn.f32x2, even with --fmad=false), so every
+// operation rounds as in the reference's SSE code.  fma(a, b, +0) equals the rounded product
+// except that an exact zero product is +0: values can differ only in the sign of a zero, which
+// cannot change a squared distance.
+__device__ __forceinline__ unsigned long long f2pack(float a, float b) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ float2 f2unpack(unsigned long long r) {
+    float2 v;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+    return v;
+}
+__device__ __forceinline__ unsigned long long f2sub(unsigned long long a, unsigned long long b) {
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ unsigned long long f2add(unsigned long long a, unsigned long long b) {
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ unsigned long long f2mul(unsigned long long a, unsigned long long b) {  // fma(a, b, +0)
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(0ull));
+    return r;
+}
+
+// Bilinear TSSD of one mapped sample (image.hpp:42-67, sweep.hpp:32-34, :99-103): channels L, a
+// packed, b scalar, each lerp `top = p00 + fx (p10 - p00)` etc. in the reference's order.
+__device__ __forceinline__ float tssd_at(const float4* __restrict__ timg, int W, int H, double u, double v, float4 ref,
+                                         float T) {
+    if (!(u >= 0.0 && v >= 0.0 && u <= W - 1.0 && v <= H - 1.0)) return T;
+    int x0 = (int)floor(u);
+    int y0 = (int)floor(v);
+    if (x0 >= W - 1) x0 = W - 2;
+    if (y0 >= H - 1) y0 = H - 2;
+    if (x0 < 0) x0 = 0;
+    if (y0 < 0) y0 = 0;
+    const float fx = (float)(u - x0);
+    const float fy = (float)(v - y0);
+    const float4* r0 = timg + ((size_t)y0 * W + x0);
+    const float4 p00 = __ldg(r0), p10 = __ldg(r0 + 1);
+    const float4 p01 = __ldg(r0 + W), p11 = __ldg(r0 + W + 1);
+    const unsigned long long FX = f2pack(fx, fx), FY = f2pack(fy, fy);
+    const unsigned long long a00 = f2pack(p00.x, p00.y), a10 = f2pack(p10.x, p10.y);
+    const unsigned long long a01 = f2pack(p01.x, p01.y), a11 = f2pack(p11.x, p11.y);
+    const unsigned long long top = f2add(a00, f2mul(FX, f2sub(a10, a00)));
+    const unsigned long long bot = f2add(a01, f2mul(FX, f2sub(a11, a01)));
+    const unsigned long long o01 = f2add(top, f2mul(FY, f2sub(bot, top)));
+    const float t2 = p00.z + fx * (p10.z - p00.z), b2 = p01.z + fx * (p11.z - p01.z);
+    const float o2 = t2 + fy * (b2 - t2);
+    // color_dist2 (image.hpp:13-16): (d0 d0 + d1 d1) + d2 d2, d = ref - sample
+    const unsigned long long d01 = f2sub(f2pack(ref.x, ref.y), o01);
+    const float2 sq = f2unpack(f2mul(d01, d01));
+    const float d2c = ref.z - o2;
+    const float dist = (sq.x + sq.y) + d2c * d2c;
+    return dist < T ? dist : T;
+}
+
 template <bool kIdR, bool kCanonK>
 __device__ __forceinline__ float sweep_sample(const Cam& rc, const Cam& tc, const float4* __restrict__ timg, int W,
                                               int H, double d, double vx, double vy, float4 ref, float T) {
@@ -65,61 +129,7 @@ __device__ __forceinline__ float sweep_sample(const Cam& rc, const Cam& tc, cons
     }
     const double u = hx / hz;
     const double v = hy / hz;
-    // ImageBuffer::contains (image.hpp:42-44)
-    if (!(u >= 0.0 && v >= 0.0 && u <= W - 1.0 && v <= H - 1.0)) return T;
-    // ImageBuffer::bilinear (image.hpp:47-67)
-    int x0 = (int)floor(u);
-    int y0 = (int)floor(v);
-    if (x0 >= W - 1) x0 = W - 2;
-    if (y0 >= H - 1) y0 = H - 2;
-    if (x0 < 0) x0 = 0;
-    if (y0 < 0) y0 = 0;
-    const float fx = (float)(u - x0);
-    const float fy = (float)(v - y0);
-    const float4* r0 = timg + (size_t)y0 * W + x0;
-    const float4 p00 = __ldg(r0), p10 = __ldg(r0 + 1);
-    const float4 p01 = __ldg(r0 + W), p11 = __ldg(r0 + W + 1);
-    float o0, o1, o2;
-    {
-        const float top = p00.x + fx * (p10.x - p00.x);
-        const float bot = p01.x + fx * (p11.x - p01.x);
-        o0 = top + fy * (bot - top);
-    }
-    {
-        const float top = p00.y + fx * (p10.y - p00.y);
-        const float bot = p01.y + fx * (p11.y - p01.y);
-        o1 = top + fy * (bot - top);
-    }
-    {
-        const float top = p00.z + fx * (p10.z - p00.z);
-        const float bot = p01.z + fx * (p11.z - p01.z);
-        o2 = top + fy * (bot - top);
-    }
-    // tssd (sweep.hpp:32-34): std::min(T, dist2)
-    const float d2 = color_dist2(ref.x, ref.y, ref.z, o0, o1, o2);
-    return d2 < T ? d2 : T;
-}
-
-// Bilinear TSSD of one mapped sample (image.hpp:47-67, sweep.hpp:32-34, :99-103).
-__device__ __forceinline__ float tssd_at(const float4* __restrict__ timg, int W, int H, double u, double v, float4 ref,
-                                         float T) {
-    if (!(u >= 0.0 && v >= 0.0 && u <= W - 1.0 && v <= H - 1.0)) return T;
-    int x0 = (int)floor(u);
-    int y0 = (int)floor(v);
-    if (x0 >= W - 1) x0 = W - 2;
-    if (y0 >= H - 1) y0 = H - 2;
-    if (x0 < 0) x0 = 0;
-    if (y0 < 0) y0 = 0;
-    const float fx = (float)(u - x0);
-    const float fy = (float)(v - y0);
-    const float4* r0 = timg + (y0 * W + x0);
-    const float4 p00 = __ldg(r0), p10 = __ldg(r0 + 1);
-    const float4 p01 = __ldg(r0 + W), p11 = __ldg(r0 + W + 1);
-    const float t0 = p00.x + fx * (p10.x - p00.x), b0 = p01.x + fx * (p11.x - p01.x);
-    const float t1 = p00.y + fx * (p10.y - p00.y), b1 = p01.y + fx * (p11.y - p01.y);
-    const float t2 = p00.z + fx * (p10.z - p00.z), b2 = p01.z + fx * (p11.z - p01.z);
-    const float d2 = color_dist2(ref.x, ref.y, ref.z, t0 + fy * (b0 - t0), t1 + fy * (b1 - t1), t2 + fy * (b2 - t2));
-    return d2 < T ? d2 : T;
+    return tssd_at(timg, W, H, u, v, ref, T);
 }
 
 // The kIdR && kCanonK inner loop over a staged chunk, for one (hypothesis, target).  With every
