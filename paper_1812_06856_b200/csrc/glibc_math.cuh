@@ -205,13 +205,6 @@ LFDG_HD double exp_nonpos(double x) {
     return fma_(scale, tmp, scale);
 }
 
-#if defined(__CUDACC__)
-// Copy the exp table into shared memory (block-cooperative); returns the smem pointer.
-__device__ __forceinline__ const uint64_t* stage_exp_table(uint64_t* smem256) {
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) smem256[i] = kExpTabDev[i];
-    return smem256;
-}
-#endif
 
 // __expf_fma (glibc sysdeps/ieee754/flt-32/e_expf.c, x86-64 FMA build).
 LFDG_HD float expf(float x) {

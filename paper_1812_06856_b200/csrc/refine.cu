@@ -174,7 +174,6 @@ struct WarpSmem {
     double m_task;  // upper bound of V_t + O_t for the current task
     int cw;         // photo-cache row width: max(32, N)
 };
-constexpr int kMaxTargets = 64;
 constexpr int kWays = 4;  // photo-cache slots per (lane, target)
 
 // rows of the photo cache: lane + t0 over the target groups (N <= 32: the 32 lanes; G = 16: one
@@ -852,13 +851,15 @@ void refine_iteration(Ctx& c, int l) {
     a.per_dir = a.radius_sp >= a.kernel_step ? a.radius_sp / a.kernel_step : 0;
     a.n_slots = 8 + 8 * a.per_dir;
     a.counters = c.counters.p;
-    if (a.N > kMaxTargets) throw Error(LFDG_INVALID_PARAMS, "too many matching views (max 64)");
     const int cap = 1 + a.n_slots + 8;  // cand[0] = the task's plane, then phase A, then phase B
     bool flat = c.identity_rot && c.canonical_k;
     for (const lfdg_camera& k : c.cams)
         flat = flat && k.t[2] == 0.0 && k.K[0] == c.cams[0].K[0] && k.K[2] == c.cams[0].K[2] &&
                k.K[4] == c.cams[0].K[4] && k.K[5] == c.cams[0].K[5];
     const size_t smem = 4 * warp_smem_bytes(a.N, flat);
+    // the per-warp target tables grow with the number of matching views: ~190 for kFlat, ~150 in
+    // general fit the 227 KB of shared memory of a CTA
+    if (smem > 227 * 1024) throw Error(LFDG_INVALID_PARAMS, "too many matching views for the refinement kernel");
     if (rn > 0) {
         // the refine gather raster from the current snapshot (labels, depth)
         k_build_raster<<<dim3(ceil_div(c.hw(), 256), c.V), 256, 0, c.stream>>>(c.labels.p, c.depth.p, c.W, c.H, c.gw,

@@ -107,3 +107,33 @@ def test_rig_fusion(rig):
     for v in range(nv):
         got = dc.get_fused(v)
         assert np.array_equal(got.view(np.uint32), want[v].view(np.uint32)), f"{kind}: fused view {v}"
+
+
+def test_many_matching_views(ref):
+    """70 views with all-others matching: N = 69 targets per view (the refinement's target groups
+    of 32 lanes and the wide photo cache), every stage bit-exact against the reference."""
+    from paper_1812_06856_b200 import api
+
+    sc = ref.render_scene("cluttered", 70, 64, 48, 64.0, 0.01)
+    rs = ref.Session(sc["lab"], sc["cams"], sc["range"])
+    dc = api.DeviceContext(0)
+    dc.set_views(sc["lab"], sc["cams"], sc["range"])
+    for v in range(70):
+        rs.slic(v, 8, 0.1, 10)
+        dc.slic(v, api.SlicParams(8, 0.1, 10))
+    for v in (0, 35, 69):
+        want = rs.sweep(v, 16, 0.05, 0, 1)
+        assert np.array_equal(dc.sweep(v, api.SweepParams(16, 0.05, 0), 1), want), f"sweep view {v}"
+    for v in range(70):
+        if v not in (0, 35, 69):
+            p = rs.sweep(v, 16, 0.05, 0, 1)
+            dc.set_planes(v, p)
+    rs.rasterize()
+    dc.rasterize()
+    rs.refine_context(16, iterations=1)
+    dc.make_refine_context(api.EnergyParams(iterations=1), 16)
+    acc_r, _ = rs.refine_iteration(1, with_stats=True)
+    acc_g, _ = dc.refine_iteration(1)
+    for v in range(70):
+        assert np.array_equal(dc.get_planes(v), rs.planes(v)), f"refine view {v}"
+    assert acc_g == acc_r
