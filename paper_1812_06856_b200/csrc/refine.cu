@@ -179,10 +179,12 @@ constexpr int kWays = 4;  // photo-cache slots per (lane, target)
 // rows of the photo cache: lane + t0 over the target groups (N <= 32: the 32 lanes; G = 16: one
 // row per (candidate slot, target); G = 32: one per target)
 __host__ __device__ inline int cache_width(int N) { return N > 32 ? (N + 31) / 32 * 32 : 32; }
+// lanes per candidate slot: a power of two >= N (at least 8), so 32 / G candidates share a warp
+__host__ __device__ inline int lanes_per_candidate(int N) { return N <= 8 ? 8 : N <= 16 ? 16 : 32; }
 __host__ __device__ inline size_t target_row_bytes(bool flat) { return flat ? sizeof(TargetFlat) : sizeof(TargetRow); }
 __host__ __device__ inline size_t warp_smem_bytes(int N, bool flat) {
     const size_t b = (size_t)(kWays + 1) * cache_width(N) * sizeof(double2) + (size_t)N * target_row_bytes(flat) +
-                     32 * sizeof(PixGeo) + 2 * (size_t)N * sizeof(double);
+                     32 * sizeof(PixGeo) + (size_t)(32 / lanes_per_candidate(N)) * N * sizeof(double);
     return (b + 127) & ~(size_t)127;
 }
 
@@ -245,7 +247,7 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
     const int lane = threadIdx.x & 31;
     const int N = a.N;
     if (N == 0) return 1.0;
-    const int G = N <= 16 ? 16 : 32;
+    const int G = lanes_per_candidate(N);
     const int cs = lane / G;  // candidate slot
     const int tl = lane % G;  // target lane
     const size_t hw = (size_t)a.W * a.H;
@@ -399,11 +401,12 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
 }
 
 // The reference's sequential greedy over cand[base, base + n) (refine.hpp:279-303) with the
-// running prune E_s (1 + eta) <= e_cur.  Candidates are evaluated two at a time when N <= 16 (one
-// per half-warp): the second one speculatively, against the running best before the first is
-// decided.  Decisions are still taken in index order with exact energies — after accepting the
-// first, the second is re-tested against the new best and dropped if the prune now rejects it (it
-// can then not be accepted either) — so the accepted planes and the count are the reference's.
+// running prune E_s (1 + eta) <= e_cur.  A warp evaluates up to 32 / G consecutive surviving
+// candidates at once (one per lane group, G = lanes_per_candidate(N)): the later ones
+// speculatively, against the running best before the earlier ones are decided.  Decisions are
+// still taken in index order with exact energies — after an acceptance the later candidates are
+// re-tested against the new best and dropped if the prune now rejects them (they can then not be
+// accepted either) — so the accepted planes and the count are the reference's.
 // init: cand[0] is the current plane and its energy initialises e_cur (refine.hpp:277).
 // current: index in cand of the running plane.
 template <bool kIdR, bool kCanonK, int kFlat>
@@ -412,7 +415,8 @@ __device__ __forceinline__ void greedy(const RefineArgs& a, const WarpSmem& w, i
                                        unsigned long long& pix_evals, unsigned& cand_evals) {
     const int lane = threadIdx.x & 31;
     const bool prune = a.use_s && a.use_c;
-    const bool pairs = a.N <= 16 && !init;
+    const int G = lanes_per_candidate(a.N);
+    const int slots = init ? 1 : 32 / G;
     int next = base;
     n += base;
     // The reference prunes with E_s (1 + eta) <= e_cur (refine.hpp:297).  Here the task's own bound
@@ -426,42 +430,43 @@ __device__ __forceinline__ void greedy(const RefineArgs& a, const WarpSmem& w, i
     };
     while (next < n) {
         const int idx = next + lane;
-        const unsigned m = __ballot_sync(LFDG_FULL_MASK, idx < n && passes(idx));
+        unsigned m = __ballot_sync(LFDG_FULL_MASK, idx < n && passes(idx));
         if (!m) {
             next += 32;
             continue;
         }
-        const int c1 = next + __ffs(m) - 1;
-        const unsigned m2 = m & (m - 1);
-        const int c2 = pairs && m2 ? next + __ffs(m2) - 1 : -1;
-        next = (c2 >= 0 ? c2 : c1) + 1;
-        double e1, e2 = 0;
+        // the next `slots` surviving candidates, in index order; lane group k evaluates the k-th
+        const int first = next + __ffs(m) - 1;
+        int cnt = 0, last = 0, mine = first;  // idle groups repeat the first candidate
+        for (int k = 0; k < slots && m; ++k) {
+            const int ck = next + __ffs(m) - 1;
+            m &= m - 1;
+            if (lane / G == k) mine = ck;
+            last = ck;
+            ++cnt;
+        }
+        next = last + 1;
+        double ec = 0;
         if (a.use_c) {
-            const double ec = consistency_pair<kIdR, kCanonK, kFlat>(
-                a, w, v, sp, w.cand[lane < 16 || c2 < 0 ? c1 : c2], m0, n_members);
-            const double ec1 = __shfl_sync(LFDG_FULL_MASK, ec, 0);
-            const double ec2 = __shfl_sync(LFDG_FULL_MASK, ec, 16);
-            e1 = prune ? w.es[c1] * ec1 : (a.use_s ? 1.0 * w.es[c1] : 1.0) * ec1;
-            if (c2 >= 0) e2 = prune ? w.es[c2] * ec2 : (a.use_s ? 1.0 * w.es[c2] : 1.0) * ec2;
-            pix_evals += (unsigned long long)a.N * n_members * (c2 >= 0 ? 2 : 1);
-        } else {
-            e1 = a.use_s ? 1.0 * w.es[c1] : 1.0;
-            if (c2 >= 0) e2 = a.use_s ? 1.0 * w.es[c2] : 1.0;
+            ec = consistency_pair<kIdR, kCanonK, kFlat>(a, w, v, sp, w.cand[mine], m0, n_members);
+            pix_evals += (unsigned long long)a.N * n_members * cnt;
         }
-        cand_evals += c2 >= 0 ? 2 : 1;
-        if (init) {
-            e_cur = e1;
-            continue;
-        }
-        if (e1 > e_cur) {
-            e_cur = e1;
-            current = c1;
-            accepted++;
-        }
-        if (c2 >= 0 && passes(c2) && e2 > e_cur) {
-            e_cur = e2;
-            current = c2;
-            accepted++;
+        cand_evals += cnt;
+        for (int k = 0; k < cnt; ++k) {
+            const int c = __shfl_sync(LFDG_FULL_MASK, mine, k * G);
+            const double eck = __shfl_sync(LFDG_FULL_MASK, ec, k * G);
+            double e;
+            if (a.use_c)
+                e = prune ? w.es[c] * eck : (a.use_s ? 1.0 * w.es[c] : 1.0) * eck;
+            else
+                e = a.use_s ? 1.0 * w.es[c] : 1.0;
+            if (init) {
+                e_cur = e;
+            } else if ((k == 0 || passes(c)) && e > e_cur) {
+                e_cur = e;
+                current = c;
+                accepted++;
+            }
         }
     }
     __syncwarp();
