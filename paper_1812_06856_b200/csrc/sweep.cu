@@ -56,19 +56,36 @@ __device__ __forceinline__ unsigned long long f2mul(unsigned long long a, unsign
     return r;
 }
 
-// Bilinear TSSD of one mapped sample (image.hpp:42-67, sweep.hpp:32-34, :99-103): channels L, a
-// packed, b scalar, each lerp `top = p00 + fx (p10 - p00)` etc. in the reference's order.
-__device__ __forceinline__ float tssd_at(const float4* __restrict__ timg, int W, int H, double u, double v, float4 ref,
-                                         float T) {
-    if (!(u >= 0.0 && v >= 0.0 && u <= W - 1.0 && v <= H - 1.0)) return T;
-    int x0 = (int)floor(u);
-    int y0 = (int)floor(v);
-    if (x0 >= W - 1) x0 = W - 2;
+// The row half of ImageBuffer::contains / bilinear (image.hpp:42-55) for sample row v: whether
+// 0 <= v <= H - 1, the clamped y0 and fy = (float)(v - y0).
+struct SampleRow {
+    bool ok;
+    int y0;
+    float fy;
+};
+__device__ __forceinline__ SampleRow sample_row(int H, double v) {
+    SampleRow r;
+    r.ok = v >= 0.0 && v <= H - 1.0;
+    int y0 = r.ok ? (int)floor(v) : 0;
     if (y0 >= H - 1) y0 = H - 2;
-    if (x0 < 0) x0 = 0;
     if (y0 < 0) y0 = 0;
+    r.y0 = y0;
+    r.fy = (float)(v - y0);
+    return r;
+}
+
+// Bilinear TSSD of one mapped sample (image.hpp:42-67, sweep.hpp:32-34, :99-103) given its row
+// half: channels L, a packed, b scalar, each lerp `top = p00 + fx (p10 - p00)` etc. in the
+// reference's order.
+__device__ __forceinline__ float tssd_row(const float4* __restrict__ timg, int W, double u, const SampleRow& row,
+                                          float4 ref, float T) {
+    if (!(u >= 0.0 && row.ok && u <= W - 1.0)) return T;
+    int x0 = (int)floor(u);
+    if (x0 >= W - 1) x0 = W - 2;
+    if (x0 < 0) x0 = 0;
+    const int y0 = row.y0;
     const float fx = (float)(u - x0);
-    const float fy = (float)(v - y0);
+    const float fy = row.fy;
     const float4* r0 = timg + ((size_t)y0 * W + x0);
     const float4 p00 = __ldg(r0), p10 = __ldg(r0 + 1);
     const float4 p01 = __ldg(r0 + W), p11 = __ldg(r0 + W + 1);
@@ -86,6 +103,11 @@ __device__ __forceinline__ float tssd_at(const float4* __restrict__ timg, int W,
     const float d2c = ref.z - o2;
     const float dist = (sq.x + sq.y) + d2c * d2c;
     return dist < T ? dist : T;
+}
+
+__device__ __forceinline__ float tssd_at(const float4* __restrict__ timg, int W, int H, double u, double v, float4 ref,
+                                         float T) {
+    return tssd_row(timg, W, u, sample_row(H, v), ref, T);
 }
 
 template <bool kIdR, bool kCanonK>
@@ -152,14 +174,23 @@ __device__ __forceinline__ double sweep_chunk_fast(double cost, const double2* _
     const double K00 = tc.K[0], K11 = tc.K[4];
     const double Kz0 = tc.K[2] * z, Kz1 = tc.K[5] * z;
     const double rz = 1.0 / z;
+    // v depends on the member's row only (ray.y; K01 = 0 under kCanonK): members are in row-major
+    // order, so the row half of the sample is recomputed only when the row changes (the branch is
+    // uniform: every thread of the CTA reads the same member)
+    double prev_ry = NAN;
+    SampleRow row{false, 0, 0.f};
     for (int i = 0; i < cn; ++i) {
         const double2 ray = s_ray[i];
+        if (!(ray.y == prev_ry)) {
+            prev_ry = ray.y;
+            const double hy = K11 * ((d * ray.y - rt1) + tt1) + Kz1;
+            const double qy = hy * rz;
+            row = sample_row(H, __fma_rn(__fma_rn(-qy, z, hy), rz, qy));
+        }
         const double hx = K00 * ((d * ray.x - rt0) + tt0) + Kz0;
-        const double hy = K11 * ((d * ray.y - rt1) + tt1) + Kz1;
-        const double qx = hx * rz, qy = hy * rz;
+        const double qx = hx * rz;
         const double u = __fma_rn(__fma_rn(-qx, z, hx), rz, qx);
-        const double v = __fma_rn(__fma_rn(-qy, z, hy), rz, qy);
-        cost += (double)tssd_at(timg, W, H, u, v, s_ref[i], T);
+        cost += (double)tssd_row(timg, W, u, row, s_ref[i], T);
     }
     return cost;
 }
