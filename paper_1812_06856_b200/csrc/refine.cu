@@ -295,8 +295,14 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
                     }
                     if ((unsigned)px >= (unsigned)a.W || (unsigned)py >= (unsigned)a.H) return false;
                     // tgrid.label(px, py) and snapshot.depth[t](px, py) (refine.hpp:146-152) in one
-                    // 16-byte gather: (label word, depth, 1 / (double)depth)
-                    rr = __ldg(ras + (unsigned)(py * a.W + px));
+                    // 16-byte gather: (label word, depth, 1 / (double)depth); kFlat == 3: the
+                    // 8-byte raster (label word, depth), 1 / depth is computed when it is needed
+                    if (kFlat == 3) {
+                        const int2 r2 = __ldg(reinterpret_cast<const int2*>(ras) + (unsigned)(py * a.W + px));
+                        rr = make_int4(r2.x, r2.y, 0, 0);
+                    } else {
+                        rr = __ldg(ras + (unsigned)(py * a.W + px));
+                    }
                     return true;
                 };
                 const PixGeo* qp = geo;  // walked as a pointer: a loop-carried register, never recomputed
@@ -326,7 +332,7 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
                     const float td = __int_as_float(r.y);
                     if (td <= 0) continue;  // no target depth: not in X or Y
                     if (zt <= (double)td * (1.0 + 1e-6)) {
-                        const double rr = inv_z - __hiloint2double(r.w, r.z);
+                        const double rr = inv_z - (kFlat == 3 ? 1.0 / (double)td : __hiloint2double(r.w, r.z));
                         vis_sum += libm::exp_nonpos(-rr * rr * a.inv_two_sigma2);
                         ++x_count;
                     } else {
@@ -565,7 +571,9 @@ __global__ void __launch_bounds__(128, LFDG_REFINE_MIN_BLOCKS) k_refine(RefineAr
                 TargetFlat& g = static_cast<TargetFlat*>(w.tg)[ti];
                 g.T0 = rel[9];
                 g.T1 = rel[10];
-                g.ras = a.ras + (size_t)t * a.W * a.H;
+                g.ras = kFlat == 3 ? reinterpret_cast<const int4*>(reinterpret_cast<const int2*>(a.ras) +
+                                                                   (size_t)t * a.W * a.H)
+                                   : a.ras + (size_t)t * a.W * a.H;
             } else {
                 TargetRow& g = static_cast<TargetRow*>(w.tg)[ti];
                 for (int k = 0; k < 9; ++k) g.R[k] = rel[k];
@@ -750,6 +758,20 @@ __global__ void k_member_rays(const int32_t* __restrict__ mpix, const Cam* cams,
     mray[(size_t)v * hw + i] = make_double2(rx, ry);
 }
 
+// The 8-byte raster of kFlat == 3 (many matching views: half the gather footprint in L2):
+// (label word, depth); 1 / depth is computed at the sample.
+__global__ void k_build_raster8(const int32_t* __restrict__ labels, const float* __restrict__ depth, int W, int H,
+                                int gw, int2* ras) {
+    const size_t hw = (size_t)W * H;
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= hw) return;
+    const int v = blockIdx.y;
+    const int lab = labels[(size_t)v * hw + i];
+    const int gx = lab % gw, gy = lab / gw;
+    ras[(size_t)v * hw + i] = make_int2(lab | (((gx & 3) | ((gy & 1) << 2)) << 28),
+                                        __float_as_int(depth[(size_t)v * hw + i]));
+}
+
 inline unsigned ceil_div(size_t a, size_t b) { return (unsigned)((a + b - 1) / b); }
 
 }  // namespace
@@ -861,14 +883,31 @@ void refine_iteration(Ctx& c, int l) {
     for (const lfdg_camera& k : c.cams)
         flat = flat && k.t[2] == 0.0 && k.K[0] == c.cams[0].K[0] && k.K[2] == c.cams[0].K[2] &&
                k.K[4] == c.cams[0].K[4] && k.K[5] == c.cams[0].K[5];
+    if (flat) {
+        a.row_inv = 1;
+        for (int vv = 0; vv < c.V; ++vv)
+            for (int i = 0; i < t.n_targets; ++i) {
+                const lfdg_camera& cv = c.cams[vv];
+                const lfdg_camera& ct = c.cams[t.targets_host[(size_t)vv * t.n_targets + i]];
+                // rel_trans.y = t_t.y - (R_rel t_v).y with R_rel = I (kFlat)
+                if (ct.t[1] - ((0.0 * cv.t[0] + 1.0 * cv.t[1]) + 0.0 * cv.t[2]) != 0.0) a.row_inv = 0;
+            }
+    }
     const size_t smem = 4 * warp_smem_bytes(a.N, flat);
     // the per-warp target tables grow with the number of matching views: ~190 for kFlat, ~150 in
     // general fit the 227 KB of shared memory of a CTA
     if (smem > 227 * 1024) throw Error(LFDG_INVALID_PARAMS, "too many matching views for the refinement kernel");
     if (rn > 0) {
         // the refine gather raster from the current snapshot (labels, depth)
-        k_build_raster<<<dim3(ceil_div(c.hw(), 256), c.V), 256, 0, c.stream>>>(c.labels.p, c.depth.p, c.W, c.H, c.gw,
-                                                                                c.ras.p);
+        // many matching views on a non-linear flat rig: the 8-byte raster (kFlat == 3) halves the
+        // gather working set (C4: 24 targets x a wide vertical disparity band)
+        const bool ras8 = flat && !a.row_inv && a.N > 16;
+        if (ras8)
+            k_build_raster8<<<dim3(ceil_div(c.hw(), 256), c.V), 256, 0, c.stream>>>(
+                c.labels.p, c.depth.p, c.W, c.H, c.gw, reinterpret_cast<int2*>(c.ras.p));
+        else
+            k_build_raster<<<dim3(ceil_div(c.hw(), 256), c.V), 256, 0, c.stream>>>(c.labels.p, c.depth.p, c.W, c.H,
+                                                                                    c.gw, c.ras.p);
         LFDG_LAUNCHED(&c);
         auto launch = [&](auto kernel) {
             LFDG_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -886,20 +925,14 @@ void refine_iteration(Ctx& c, int l) {
         // kFlat (flat above): every rotation I, canonical and identical K, every camera centre at
         // z = 0 (then every rel_trans.z = 0): the rectified / grid rigs of the fixtures.
         if (flat) {
-            a.row_inv = 1;
-            for (int vv = 0; vv < c.V; ++vv)
-                for (int i = 0; i < t.n_targets; ++i) {
-                    const lfdg_camera& cv = c.cams[vv];
-                    const lfdg_camera& ct = c.cams[t.targets_host[(size_t)vv * t.n_targets + i]];
-                    // rel_trans.y = t_t.y - (R_rel t_v).y with R_rel = I (kFlat)
-                    if (ct.t[1] - ((0.0 * cv.t[0] + 1.0 * cv.t[1]) + 0.0 * cv.t[2]) != 0.0) a.row_inv = 0;
-                }
             a.uK00 = c.cams[0].K[0];
             a.uK02 = c.cams[0].K[2];
             a.uK11 = c.cams[0].K[4];
             a.uK12 = c.cams[0].K[5];
             if (a.row_inv)
                 launch(k_refine<true, true, 2>);
+            else if (ras8)
+                launch(k_refine<true, true, 3>);
             else
                 launch(k_refine<true, true, 1>);
         } else if (c.identity_rot && c.canonical_k) {
