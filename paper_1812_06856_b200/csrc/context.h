@@ -88,6 +88,7 @@ struct SlicScratch {
     DevBuf<int> adj_cnt, adj_off, adj_cur, adj, g_count, g_merged;
     DevBuf<unsigned char> g_assigned;
     DevBuf<int> bbox, lcnt, moff_b, queue, seen;
+    DevBuf<int> abox;  // [n][nsp][4] bbox of each cluster's pixels in the current assignment
 };
 struct RefineScratch {
     DevBuf<double2> mray;      // [V][H*W] member rays in CSR order

@@ -57,7 +57,7 @@ __global__ void k_slic_init(const float4* __restrict__ lab, int W, int H, int S,
 __global__ void __launch_bounds__(128) k_slic_assign(const float4* __restrict__ lab, int W, int H, int S, int gw,
                                                      int gh, float spatial_w, int v0, const double* __restrict__ ccx,
                                                      const double* __restrict__ ccy,
-                                                     const float4* __restrict__ ccol, int32_t* labels) {
+                                                     const float4* __restrict__ ccol, int32_t* labels, int* abox) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y;
     const int b = blockIdx.z;
@@ -98,6 +98,18 @@ __global__ void __launch_bounds__(128) k_slic_assign(const float4* __restrict__ 
         }
     }
     labels[(size_t)(v0 + b) * hw + (size_t)y * W + x] = best;
+    // the cluster's pixel bbox for k_slic_update, as four minima (x, y, -x, -y); the lanes of a
+    // warp share y and have consecutive x, so one lane per label of the warp updates it
+    const unsigned am = __activemask();
+    const unsigned peers = __match_any_sync(am, best);
+    const int lane = threadIdx.x & 31;
+    if (lane == __ffs(peers) - 1) {
+        int* bx = abox + ((size_t)b * nsp + best) * 4;
+        atomicMin(bx + 0, x);
+        atomicMin(bx + 1, y);
+        atomicMin(bx + 2, -(x - lane + (31 - __clz(peers))));
+        atomicMin(bx + 3, -y);
+    }
 }
 
 // ---------------------------------------------------------------- update --------------
@@ -107,7 +119,7 @@ __global__ void __launch_bounds__(128) k_slic_assign(const float4* __restrict__ 
 __global__ void __launch_bounds__(256) k_slic_update(const float4* __restrict__ lab,
                                                      const int32_t* __restrict__ labels, int W, int H, int S,
                                                      int gw, int gh, int v0, double* ccx, double* ccy,
-                                                     float4* ccol) {
+                                                     float4* ccol, const int* __restrict__ abox) {
     const int nsp = gw * gh;
     const int id = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -116,9 +128,11 @@ __global__ void __launch_bounds__(256) k_slic_update(const float4* __restrict__ 
     const size_t hw = (size_t)W * H;
     const int32_t* lb = labels + (size_t)(v0 + b) * hw;
     const float4* im = lab + (size_t)(v0 + b) * hw;
-    const int gx = id % gw, gy = id / gw;
-    const int xa = max(0, (gx - 2) * S), xb = min(W, (gx + 3) * S);
-    const int ya = max(0, (gy - 2) * S), yb = min(H, (gy + 3) * S);
+    // the members lie in the cluster's assignment bbox (k_slic_assign), itself inside the window
+    // of cells [gx-2, gx+2] x [gy-2, gy+2]; empty bbox: no members
+    const int* bx = abox + ((size_t)b * nsp + id) * 4;
+    const int xa = max(0, bx[0]), xb = min(W, 1 - bx[2]);
+    const int ya = max(0, bx[1]), yb = min(H, 1 - bx[3]);
     long long sx = 0, sy = 0;
     int cnt = 0;
     double s0 = 0, s1 = 0, s2 = 0;
@@ -715,12 +729,15 @@ void slic_views(Ctx& c, int v0, int n, const lfdg_slic_params& p) {
                                                                 s.ccol.p);
     LFDG_LAUNCHED(&c);
     const float spatial_w = p.compactness / static_cast<float>(S);
+    s.abox.alloc((size_t)n * nsp * 4);
     for (int it = 0; it < p.iterations; ++it) {
+        LFDG_CUDA_CHECK(cudaMemsetAsync(s.abox.p, 0x7f, (size_t)n * nsp * 4 * sizeof(int), st));  // empty boxes
         k_slic_assign<<<dim3(ceil_div(W, 128), H, n), 128, 0, st>>>(c.lab.p, W, H, S, gw, gh, spatial_w, v0, s.ccx.p,
-                                                                     s.ccy.p, s.ccol.p, c.labels.p);
+                                                                     s.ccy.p, s.ccol.p, c.labels.p, s.abox.p);
         LFDG_LAUNCHED(&c);
         k_slic_update<<<dim3(ceil_div((size_t)nsp * 32, 256), n), 256, 0, st>>>(c.lab.p, c.labels.p, W, H, S, gw, gh,
-                                                                               v0, s.ccx.p, s.ccy.p, s.ccol.p);
+                                                                               v0, s.ccx.p, s.ccy.p, s.ccol.p,
+                                                                               s.abox.p);
         LFDG_LAUNCHED(&c);
     }
 
