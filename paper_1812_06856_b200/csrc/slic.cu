@@ -133,33 +133,39 @@ __global__ void __launch_bounds__(256) k_slic_update(const float4* __restrict__ 
     const int* bx = abox + ((size_t)b * nsp + id) * 4;
     const int xa = max(0, bx[0]), xb = min(W, 1 - bx[2]);
     const int ya = max(0, bx[1]), yb = min(H, 1 - bx[3]);
+    // colour sums: lane k < 3 owns channel k's sequential sum; each step's member colours are
+    // staged in shared memory and added in ascending lane (= row-major pixel) order
+    __shared__ float4 s_col[8][32];
+    float4* buf = s_col[(threadIdx.x >> 5) & 7];
+    const float* bch = reinterpret_cast<const float*>(buf) + (lane < 3 ? lane : 0);
     long long sx = 0, sy = 0;
     int cnt = 0;
-    double s0 = 0, s1 = 0, s2 = 0;
+    double sc = 0;  // this lane's channel sum (lanes 0-2)
     for (int y = ya; y < yb; ++y) {
         for (int xc = xa; xc < xb; xc += 32) {
             const int x = xc + lane;
             const bool m = x < xb && lb[(size_t)y * W + x] == id;
             unsigned mask = __ballot_sync(LFDG_FULL_MASK, m);
             if (!mask) continue;
-            float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (m) c = im[(size_t)y * W + x];
+            if (m) buf[lane] = im[(size_t)y * W + x];
             const int n = __popc(mask);
             sx += __reduce_add_sync(LFDG_FULL_MASK, m ? (unsigned)x : 0u);
             sy += (long long)y * n;
             cnt += n;
-            while (mask) {
-                const int j = __ffs(mask) - 1;
-                mask &= mask - 1;
-                const float a0 = __shfl_sync(LFDG_FULL_MASK, c.x, j);
-                const float a1 = __shfl_sync(LFDG_FULL_MASK, c.y, j);
-                const float a2 = __shfl_sync(LFDG_FULL_MASK, c.z, j);
-                s0 += (double)a0;
-                s1 += (double)a1;
-                s2 += (double)a2;
+            __syncwarp();
+            if (lane < 3) {
+                while (mask) {
+                    const int j = __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    sc += (double)bch[4 * j];
+                }
             }
+            __syncwarp();
         }
     }
+    const double s0 = sc;
+    const double s1 = __shfl_sync(LFDG_FULL_MASK, sc, 1);
+    const double s2 = __shfl_sync(LFDG_FULL_MASK, sc, 2);
     if (lane == 0 && cnt > 0) {
         const size_t o = (size_t)b * nsp + id;
         ccx[o] = (double)sx / cnt;
