@@ -168,13 +168,15 @@ struct WarpSmem {
     double* es;     // [cap]   (global scratch)
     void* tg;       // [N] TargetRow, or TargetFlat for kFlat
     PixGeo* geo;    // [32] geometry of the current pixel chunk (one entry per lane)
-    double2* pc;    // [cw][kWays + 1] lane-private photo-weight cache rows: (weight, raster word); the
+    double2* pc;    // [cw][ways + 1] lane-private photo-weight cache rows: (weight, raster word); the
                     // pad entry staggers the rows over the banks
     double* res;    // [2][N] V + O per target, per candidate slot
     double m_task;  // upper bound of V_t + O_t for the current task
     int cw;         // photo-cache row width: max(32, N)
 };
-constexpr int kWays = 4;  // photo-cache slots per (lane, target)
+// photo-cache slots per (lane, target): 4, or 2 in the 8-byte-raster mode (kFlat == 3: many
+// targets, where the L1 capacity the cache would take matters more than the cache hits)
+__host__ __device__ constexpr int cache_ways(int flat_mode) { return flat_mode == 3 ? 2 : 4; }
 
 // rows of the photo cache: lane + t0 over the target groups (N <= 32: the 32 lanes; G = 16: one
 // row per (candidate slot, target); G = 32: one per target)
@@ -182,8 +184,9 @@ __host__ __device__ inline int cache_width(int N) { return N > 32 ? (N + 31) / 3
 // lanes per candidate slot: a power of two >= N (at least 8), so 32 / G candidates share a warp
 __host__ __device__ inline int lanes_per_candidate(int N) { return N <= 8 ? 8 : N <= 16 ? 16 : 32; }
 __host__ __device__ inline size_t target_row_bytes(bool flat) { return flat ? sizeof(TargetFlat) : sizeof(TargetRow); }
-__host__ __device__ inline size_t warp_smem_bytes(int N, bool flat) {
-    const size_t b = (size_t)(kWays + 1) * cache_width(N) * sizeof(double2) + (size_t)N * target_row_bytes(flat) +
+__host__ __device__ inline size_t warp_smem_bytes(int N, int flat_mode) {
+    const size_t b = (size_t)(cache_ways(flat_mode) + 1) * cache_width(N) * sizeof(double2) +
+                     (size_t)N * target_row_bytes(flat_mode != 0) +
                      32 * sizeof(PixGeo) + (size_t)(32 / lanes_per_candidate(N)) * N * sizeof(double);
     return (b + 127) & ~(size_t)127;
 }
@@ -261,7 +264,7 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
     for (int t0 = 0; t0 < N; t0 += G) {
         const int t = t0 + tl;
         const bool act = t < N;
-        double2* const pcl = w.pc + (lane + t0) * (kWays + 1);  // this lane's cache row
+        double2* const pcl = w.pc + (lane + t0) * (cache_ways(kFlat) + 1);  // this lane's cache row
         double T0 = 0, T1 = 0;
         const int4* ras = nullptr;
         if (kFlat && act) {
@@ -316,7 +319,7 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
                     if (!valid) continue;
                     const double zt = qc->sv2, inv_z = qc->f_inv;
                     if (r.x != cached_word) {  // refine.hpp:147-150
-                        const int way = (((unsigned)r.x >> 28) + 2 * ((unsigned)r.x >> 30)) & (kWays - 1);
+                        const int way = (((unsigned)r.x >> 28) + 2 * ((unsigned)r.x >> 30)) & (cache_ways(kFlat) - 1);
                         double2* e = pcl + way;
                         const double2 c = *e;
                         if (__double2loint(c.y) == r.x) {
@@ -367,7 +370,7 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
                     if ((unsigned)px >= (unsigned)a.W || (unsigned)py >= (unsigned)a.H) continue;
                     const int4 r = __ldg(g.ras + (unsigned)(py * a.W + px));
                     if (r.x != cached_word) {  // refine.hpp:147-150
-                        const int way = (((unsigned)r.x >> 28) + 2 * ((unsigned)r.x >> 30)) & (kWays - 1);
+                        const int way = (((unsigned)r.x >> 28) + 2 * ((unsigned)r.x >> 30)) & (cache_ways(kFlat) - 1);
                         double2* e = pcl + way;
                         const double2 c = *e;
                         if (__double2loint(c.y) == r.x) {
@@ -533,7 +536,7 @@ __global__ void __launch_bounds__(128, LFDG_REFINE_MIN_BLOCKS) k_refine(RefineAr
     WarpSmem w;
     w.cw = cache_width(a.N);
     w.pc = reinterpret_cast<double2*>(base);
-    w.tg = base + (size_t)(kWays + 1) * w.cw * sizeof(double2);
+    w.tg = base + (size_t)(cache_ways(kFlat) + 1) * w.cw * sizeof(double2);
     w.geo = reinterpret_cast<PixGeo*>(static_cast<unsigned char*>(w.tg) + (size_t)a.N * target_row_bytes(kFlat));
     w.res = reinterpret_cast<double*>(w.geo + 32);
     w.cand = g_cand + (size_t)gwarp * cap;
@@ -587,7 +590,7 @@ __global__ void __launch_bounds__(128, LFDG_REFINE_MIN_BLOCKS) k_refine(RefineAr
                 g.ras = a.ras + (size_t)t * a.W * a.H;
             }
         }
-        for (int k = lane; k < (kWays + 1) * w.cw; k += 32)  // new reference colour: empty photo cache
+        for (int k = lane; k < (cache_ways(kFlat) + 1) * w.cw; k += 32)  // new reference colour: empty photo cache
             w.pc[k] = make_double2(0.0, __hiloint2double(-1, -1));
         __syncwarp();
 
@@ -893,7 +896,10 @@ void refine_iteration(Ctx& c, int l) {
                 if (ct.t[1] - ((0.0 * cv.t[0] + 1.0 * cv.t[1]) + 0.0 * cv.t[2]) != 0.0) a.row_inv = 0;
             }
     }
-    const size_t smem = 4 * warp_smem_bytes(a.N, flat);
+    // kFlat mode: 2 linear rig (row-invariant targets), 3 many targets with the 8-byte raster,
+    // 1 other flat rigs, 0 general
+    const int flat_mode = !flat ? 0 : a.row_inv ? 2 : a.N > 16 ? 3 : 1;
+    const size_t smem = 4 * warp_smem_bytes(a.N, flat_mode);
     // the per-warp target tables grow with the number of matching views: ~190 for kFlat, ~150 in
     // general fit the 227 KB of shared memory of a CTA
     if (smem > 227 * 1024) throw Error(LFDG_INVALID_PARAMS, "too many matching views for the refinement kernel");
@@ -901,7 +907,7 @@ void refine_iteration(Ctx& c, int l) {
         // the refine gather raster from the current snapshot (labels, depth)
         // many matching views on a non-linear flat rig: the 8-byte raster (kFlat == 3) halves the
         // gather working set (C4: 24 targets x a wide vertical disparity band)
-        const bool ras8 = flat && !a.row_inv && a.N > 16;
+        const bool ras8 = flat_mode == 3;
         if (ras8)
             k_build_raster8<<<dim3(ceil_div(c.hw(), 256), c.V), 256, 0, c.stream>>>(
                 c.labels.p, c.depth.p, c.W, c.H, c.gw, reinterpret_cast<int2*>(c.ras.p));
