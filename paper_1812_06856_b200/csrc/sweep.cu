@@ -149,8 +149,12 @@ __device__ __forceinline__ float sweep_sample(const Cam& rc, const Cam& tc, cons
         hy = (tc.K[3] * c0 + tc.K[4] * c1) + tc.K[5] * c2;
         hz = (tc.K[6] * c0 + tc.K[7] * c1) + tc.K[8] * c2;
     }
-    const double u = hx / hz;
-    const double v = hy / hz;
+    // u = hx / hz, v = hy / hz: one correctly rounded reciprocal and a Markstein correction per
+    // quotient, which yields the correctly rounded quotient (as in sweep_chunk_fast)
+    const double rz = 1.0 / hz;
+    const double qx = hx * rz, qy = hy * rz;
+    const double u = __fma_rn(__fma_rn(-qx, hz, hx), rz, qx);
+    const double v = __fma_rn(__fma_rn(-qy, hz, hy), rz, qy);
     return tssd_at(timg, W, H, u, v, ref, T);
 }
 
