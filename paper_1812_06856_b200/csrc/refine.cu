@@ -522,12 +522,13 @@ __device__ void smoothness_all(const RefineArgs& a, const WarpSmem& w, int base,
 
 // Persistent kernel: each warp pulls (view, superpixel) tasks from a global counter and runs
 // refine_iteration's task body (refine.hpp:269-320) for it.
+// Resident CTAs per SM (register budget): 8 (64 registers), or 7 in the many-target mode,
+// whose latency-bound gathers gain more from the registers and the L1 than from an 8th CTA
+// (C4: 111 -> 100 ms/view; C3 prefers 8: 104.7 vs 106.8 ms per refine launch).
+__host__ __device__ constexpr int refine_min_blocks(int flat_mode) { return flat_mode == 3 ? 7 : 8; }
 template <bool kIdR, bool kCanonK, int kFlat>
-#ifndef LFDG_REFINE_MIN_BLOCKS
-#define LFDG_REFINE_MIN_BLOCKS 8
-#endif
-__global__ void __launch_bounds__(128, LFDG_REFINE_MIN_BLOCKS) k_refine(RefineArgs a, int n_tasks, int* task_counter, int cap,
-                                                double4* g_cand, double* g_es) {
+__global__ void __launch_bounds__(128, refine_min_blocks(kFlat))
+    k_refine(RefineArgs a, int n_tasks, int* task_counter, int cap, double4* g_cand, double* g_es) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
