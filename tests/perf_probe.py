@@ -14,6 +14,7 @@ sys.path.insert(0, ROOT)
 CONFIGS = {
     "C1": dict(kind="cluttered", n=3, w=320, h=240, f=320.0, b=0.1, S=12, L=32, iters=3, K=0),
     "C2": dict(kind="cluttered", n=8, w=1024, h=768, f=1024.0, b=0.05, S=12, L=128, iters=5, K=0),
+    "C3s": dict(kind="cluttered", n=16, w=480, h=270, f=480.0, b=0.04, S=16, L=64, iters=2, K=0),
     "C3": dict(kind="cluttered", n=16, w=1920, h=1080, f=1920.0, b=0.04, S=16, L=256, iters=5, K=0),
 }
 
@@ -47,7 +48,7 @@ def main():
             t = time.time()
             acc, _ = dc.refine_iteration(l)
             dc.rasterize(); dc.synchronize()
-            marks[f"refine{l}"] = (time.time() - t, acc)
+            marks[f"refine{l}"] = (round(time.time() - t, 4), acc, dc.refine_work(reset=True))
         print(rep, marks, flush=True)
 
 
