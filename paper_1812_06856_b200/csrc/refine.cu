@@ -172,22 +172,30 @@ struct WarpSmem {
                     // pad entry staggers the rows over the banks
     double* res;    // [2][N] V + O per target, per candidate slot
     double m_task;  // upper bound of V_t + O_t for the current task
-    int cw;         // photo-cache row width: max(32, N)
+    int cw;         // photo-cache rows: one per (candidate slot, target lane of a round)
 };
 // photo-cache slots per (lane, target): 4, or 2 in the 8-byte-raster mode (kFlat == 3: many
 // targets, where the L1 capacity the cache would take matters more than the cache hits)
 __host__ __device__ constexpr int cache_ways(int flat_mode) { return flat_mode == 3 ? 2 : 4; }
 
-// rows of the photo cache: lane + t0 over the target groups (N <= 32: the 32 lanes; G = 16: one
-// row per (candidate slot, target); G = 32: one per target)
-__host__ __device__ inline int cache_width(int N) { return N > 32 ? (N + 31) / 32 * 32 : 32; }
-// lanes per candidate slot: a power of two >= N (at least 8), so 32 / G candidates share a warp
-__host__ __device__ inline int lanes_per_candidate(int N) { return N <= 8 ? 8 : N <= 16 ? 16 : 32; }
+// lanes per candidate slot G (8, 16 or 32; 32 / G candidates share a warp): the smallest power
+// of two >= N with at least 8 lanes, except in the many-target mode (flat_mode 3) for 17..24
+// targets, where 8 lanes over three target rounds keep every lane busy (one 32-lane group would
+// leave a quarter or more of them idle: C4, N = 24: 100.1 -> 91.0 ms/view)
+__host__ __device__ inline int lanes_per_candidate(int N, int flat_mode) {
+    return N <= 8 ? 8 : N <= 16 ? 16 : flat_mode == 3 && N <= 24 ? 8 : 32;
+}
+// rows of the photo cache: one per (candidate slot, target rounded up to whole rounds of G);
+// except in flat_mode 3 this is lane + t0 (N <= G, or G = 32)
+__host__ __device__ inline int cache_width(int N, int flat_mode) {
+    const int G = lanes_per_candidate(N, flat_mode);
+    return 32 / G * ((N + G - 1) / G * G);
+}
 __host__ __device__ inline size_t target_row_bytes(bool flat) { return flat ? sizeof(TargetFlat) : sizeof(TargetRow); }
 __host__ __device__ inline size_t warp_smem_bytes(int N, int flat_mode) {
-    const size_t b = (size_t)(cache_ways(flat_mode) + 1) * cache_width(N) * sizeof(double2) +
+    const size_t b = (size_t)(cache_ways(flat_mode) + 1) * cache_width(N, flat_mode) * sizeof(double2) +
                      (size_t)N * target_row_bytes(flat_mode != 0) +
-                     32 * sizeof(PixGeo) + (size_t)(32 / lanes_per_candidate(N)) * N * sizeof(double);
+                     32 * sizeof(PixGeo) + (size_t)(32 / lanes_per_candidate(N, flat_mode)) * N * sizeof(double);
     return (b + 127) & ~(size_t)127;
 }
 
@@ -250,7 +258,7 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
     const int lane = threadIdx.x & 31;
     const int N = a.N;
     if (N == 0) return 1.0;
-    const int G = lanes_per_candidate(N);
+    const int G = lanes_per_candidate(N, kFlat);
     const int cs = lane / G;  // candidate slot
     const int tl = lane % G;  // target lane
     const size_t hw = (size_t)a.W * a.H;
@@ -264,7 +272,8 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
     for (int t0 = 0; t0 < N; t0 += G) {
         const int t = t0 + tl;
         const bool act = t < N;
-        double2* const pcl = w.pc + (lane + t0) * (cache_ways(kFlat) + 1);  // this lane's cache row
+        double2* const pcl =  // this lane's cache row
+            w.pc + (kFlat == 3 ? cs * ((N + G - 1) / G * G) + t : lane + t0) * (cache_ways(kFlat) + 1);
         double T0 = 0, T1 = 0;
         const int4* ras = nullptr;
         if (kFlat && act) {
@@ -411,7 +420,7 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
 
 // The reference's sequential greedy over cand[base, base + n) (refine.hpp:279-303) with the
 // running prune E_s (1 + eta) <= e_cur.  A warp evaluates up to 32 / G consecutive surviving
-// candidates at once (one per lane group, G = lanes_per_candidate(N)): the later ones
+// candidates at once (one per lane group, G = lanes_per_candidate): the later ones
 // speculatively, against the running best before the earlier ones are decided.  Decisions are
 // still taken in index order with exact energies — after an acceptance the later candidates are
 // re-tested against the new best and dropped if the prune now rejects them (they can then not be
@@ -424,7 +433,7 @@ __device__ __forceinline__ void greedy(const RefineArgs& a, const WarpSmem& w, i
                                        unsigned long long& pix_evals, unsigned& cand_evals) {
     const int lane = threadIdx.x & 31;
     const bool prune = a.use_s && a.use_c;
-    const int G = lanes_per_candidate(a.N);
+    const int G = lanes_per_candidate(a.N, kFlat);
     const int slots = init ? 1 : 32 / G;
     int next = base;
     n += base;
@@ -535,7 +544,7 @@ __global__ void __launch_bounds__(128, refine_min_blocks(kFlat))
     const int gwarp = blockIdx.x * 4 + warp;
     unsigned char* base = smem_raw + warp * warp_smem_bytes(a.N, kFlat);
     WarpSmem w;
-    w.cw = cache_width(a.N);
+    w.cw = cache_width(a.N, kFlat);
     w.pc = reinterpret_cast<double2*>(base);
     w.tg = base + (size_t)(cache_ways(kFlat) + 1) * w.cw * sizeof(double2);
     w.geo = reinterpret_cast<PixGeo*>(static_cast<unsigned char*>(w.tg) + (size_t)a.N * target_row_bytes(kFlat));

@@ -109,23 +109,28 @@ def test_rig_fusion(rig):
         assert np.array_equal(got.view(np.uint32), want[v].view(np.uint32)), f"{kind}: fused view {v}"
 
 
-def test_many_matching_views(ref):
-    """70 views with all-others matching: N = 69 targets per view (the refinement's target groups
-    of 32 lanes and the wide photo cache), every stage bit-exact against the reference."""
+@pytest.mark.parametrize("grid", [(4, 5), (0, 0)])
+def test_many_matching_views(ref, grid):
+    """All-others matching with many targets, every stage bit-exact against the reference:
+    a 4x5 grid rig, N = 19 (the many-target mode: groups of 8 lanes over three target rounds, the
+    last one partial), and 70 views on a line, N = 69 (groups of 32 lanes over three rounds, the
+    wide photo cache)."""
     from paper_1812_06856_b200 import api
 
-    sc = ref.render_scene("cluttered", 70, 64, 48, 64.0, 0.01)
+    sc = ref.render_scene("cluttered", 70, 64, 48, 64.0, 0.01, grid=grid)
+    nv = sc["lab"].shape[0]
     rs = ref.Session(sc["lab"], sc["cams"], sc["range"])
     dc = api.DeviceContext(0)
     dc.set_views(sc["lab"], sc["cams"], sc["range"])
-    for v in range(70):
+    for v in range(nv):
         rs.slic(v, 8, 0.1, 10)
         dc.slic(v, api.SlicParams(8, 0.1, 10))
-    for v in (0, 35, 69):
+    checked = (0, nv // 2, nv - 1)
+    for v in checked:
         want = rs.sweep(v, 16, 0.05, 0, 1)
         assert np.array_equal(dc.sweep(v, api.SweepParams(16, 0.05, 0), 1), want), f"sweep view {v}"
-    for v in range(70):
-        if v not in (0, 35, 69):
+    for v in range(nv):
+        if v not in checked:
             p = rs.sweep(v, 16, 0.05, 0, 1)
             dc.set_planes(v, p)
     rs.rasterize()
@@ -134,6 +139,6 @@ def test_many_matching_views(ref):
     dc.make_refine_context(api.EnergyParams(iterations=1), 16)
     acc_r, _ = rs.refine_iteration(1, with_stats=True)
     acc_g, _ = dc.refine_iteration(1)
-    for v in range(70):
+    for v in range(nv):
         assert np.array_equal(dc.get_planes(v), rs.planes(v)), f"refine view {v}"
     assert acc_g == acc_r
