@@ -15,6 +15,8 @@ CONFIGS = {
     "C1": dict(kind="cluttered", n=3, w=320, h=240, f=320.0, b=0.1, S=12, L=32, iters=3, K=0),
     "C2": dict(kind="cluttered", n=8, w=1024, h=768, f=1024.0, b=0.05, S=12, L=128, iters=5, K=0),
     "C3s": dict(kind="cluttered", n=16, w=480, h=270, f=480.0, b=0.04, S=16, L=64, iters=2, K=0),
+    "C4": dict(kind="cluttered", n=25, w=1920, h=1080, f=1920.0, b=0.04, S=16, L=256, iters=5, K=0, grid=(5, 5)),
+    "C5": dict(kind="cluttered", n=64, w=1920, h=1080, f=1920.0, b=0.02, S=16, L=256, iters=5, K=8),
     "C3": dict(kind="cluttered", n=16, w=1920, h=1080, f=1920.0, b=0.04, S=16, L=256, iters=5, K=0),
 }
 
@@ -27,11 +29,11 @@ def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "C1"
     c = CONFIGS[name]
     t0 = time.time()
-    sc = ref.render_scene(c["kind"], c["n"], c["w"], c["h"], c["f"], c["b"])
+    sc = ref.render_scene(c["kind"], c["n"], c["w"], c["h"], c["f"], c["b"], grid=c.get("grid", (0, 0)))
     print(f"render {time.time() - t0:.1f}s", flush=True)
     dc = api.DeviceContext(0)
     dc.set_views(sc["lab"], sc["cams"], sc["range"])
-    V = c["n"]
+    V = sc["lab"].shape[0]
     ev = lambda: torch.cuda.Event(enable_timing=True)
     for rep in range(2):
         marks = {}
