@@ -282,7 +282,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     for _ in range(args.steps):
         hp.run()
     e1.record(stream)
-    torch.cuda.synchronize()
+    barrier()
     clocks = sampler.stop()
     hp.ctx.refine_iteration = orig_refine
     launches = hp.ctx.launch_count() - launches0
