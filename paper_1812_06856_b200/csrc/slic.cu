@@ -61,14 +61,28 @@ __global__ void __launch_bounds__(128) k_slic_assign(const float4* __restrict__ 
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int y = blockIdx.y;
     const int b = blockIdx.z;
-    if (x >= W) return;
     const int nsp = gw * gh;
     const size_t hw = (size_t)W * H;
+    // The block's candidate centres (one image row, <= 128 consecutive pixels: cells
+    // [gxb0, gxb1] x [gy0, gy1]) staged in shared memory once instead of read per pixel
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int pgy = y / S;
+    const int gy0 = max(0, pgy - 2), gy1 = min(gh - 1, pgy + 2);
+    const int xb = blockIdx.x * blockDim.x;
+    const int gxb0 = max(0, xb / S - 2), gxb1 = min(gw - 1, min(W - 1, xb + (int)blockDim.x - 1) / S + 2);
+    const int wb = gxb1 - gxb0 + 1;
+    const int ne = (gy1 - gy0 + 1) * wb;
+    double2* s_c = reinterpret_cast<double2*>(smem);
+    float4* s_col = reinterpret_cast<float4*>(s_c + ne);
+    for (int e = threadIdx.x; e < ne; e += blockDim.x) {
+        const int id = (gy0 + e / wb) * gw + gxb0 + e % wb;
+        s_c[e] = make_double2(ccx[(size_t)b * nsp + id], ccy[(size_t)b * nsp + id]);
+        s_col[e] = ccol[(size_t)b * nsp + id];
+    }
+    __syncthreads();
+    if (x >= W) return;
     const float4 pc = lab[(size_t)(v0 + b) * hw + (size_t)y * W + x];
-    const double* cxb = ccx + (size_t)b * nsp;
-    const double* cyb = ccy + (size_t)b * nsp;
-    const float4* ccb = ccol + (size_t)b * nsp;
-    const int pgx = x / S, pgy = y / S;
+    const int pgx = x / S;
     const float two_s = 2.f * S;
     // ds = (float)sqrt(D) > 2S is decided on D alone outside a +-2^-20 band around (2S)^2: there
     // the float rounding of the square root cannot move ds across 2S (ulp(2S) <= 2^-23 2S), so
@@ -76,18 +90,19 @@ __global__ void __launch_bounds__(128) k_slic_assign(const float4* __restrict__ 
     const double d_far = (double)two_s * two_s * (1.0 + 0x1p-20);
     float best_d = 0.f, best_s = 0.f;
     int best = -1;
-    const int gy0 = max(0, pgy - 2), gy1 = min(gh - 1, pgy + 2);
     const int gx0 = max(0, pgx - 2), gx1 = min(gw - 1, pgx + 2);
     for (int gy = gy0; gy <= gy1; ++gy) {
         for (int gx = gx0; gx <= gx1; ++gx) {
             const int id = gy * gw + gx;
-            const double ddx = (double)x - cxb[id];
-            const double ddy = (double)y - cyb[id];
+            const int e = (gy - gy0) * wb + (gx - gxb0);
+            const double2 cc = s_c[e];
+            const double ddx = (double)x - cc.x;
+            const double ddy = (double)y - cc.y;
             const double D = ddx * ddx + ddy * ddy;
             if (D > d_far) continue;  // ds > 2S for sure
             const float ds = (float)sqrt(D);
             if (ds > two_s) continue;
-            const float4 c = ccb[id];
+            const float4 c = s_col[e];
             const float dc = sqrtf(color_dist2(pc.x, pc.y, pc.z, c.x, c.y, c.z));
             const float d = dc + spatial_w * ds;
             if (best < 0 || d < best_d || (d == best_d && ds < best_s)) {
@@ -736,9 +751,13 @@ void slic_views(Ctx& c, int v0, int n, const lfdg_slic_params& p) {
     LFDG_LAUNCHED(&c);
     const float spatial_w = p.compactness / static_cast<float>(S);
     s.abox.alloc((size_t)n * nsp * 4);
+    // staged centres of one assign block: <= 128 / S + 6 cells per row band, 5 band rows
+    const size_t assign_smem = (size_t)(128 / S + 6) * 5 * (sizeof(double2) + sizeof(float4));
+    if (assign_smem > 48 * 1024)
+        LFDG_CUDA_CHECK(cudaFuncSetAttribute(k_slic_assign, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)assign_smem));
     for (int it = 0; it < p.iterations; ++it) {
         LFDG_CUDA_CHECK(cudaMemsetAsync(s.abox.p, 0x7f, (size_t)n * nsp * 4 * sizeof(int), st));  // empty boxes
-        k_slic_assign<<<dim3(ceil_div(W, 128), H, n), 128, 0, st>>>(c.lab.p, W, H, S, gw, gh, spatial_w, v0, s.ccx.p,
+        k_slic_assign<<<dim3(ceil_div(W, 128), H, n), 128, assign_smem, st>>>(c.lab.p, W, H, S, gw, gh, spatial_w, v0, s.ccx.p,
                                                                      s.ccy.p, s.ccol.p, c.labels.p, s.abox.p);
         LFDG_LAUNCHED(&c);
         k_slic_update<<<dim3(ceil_div((size_t)nsp * 32, 256), n), 256, 0, st>>>(c.lab.p, c.labels.p, W, H, S, gw, gh,
