@@ -2,22 +2,27 @@
 // (refine.hpp:253-323) with the full energy E = E_s * E_c (smoothness_term :84, pair_stats
 // :111, consistency_term :189, energy :201, normal_candidates :213).
 //
-// One CTA per (view, superpixel) task.  The reference's per-task control flow is a sequential
-// greedy over an ordered candidate list (propagation candidates in grid_neighbors(Kernel) order,
-// then the triangle normals at the phase-A depth) that accepts a candidate iff its energy is
-// strictly above the running best, pruning candidates whose upper bound E_s * (1 + eta) cannot
-// beat it.  The CTA reproduces it exactly:
-//   * the candidate list is enumerated in the reference order (ordered block compaction);
-//   * E_s of every candidate is computed in parallel (one thread per candidate);
-//   * candidates are evaluated in chunks, in order, against the running best at chunk
-//     formation (a lower bound of the reference's running best, so every candidate the
-//     reference evaluates is evaluated here); within a chunk one thread per (candidate,
-//     target) pair runs pair_stats' member loop in the reference's pixel order, so every
-//     FP64 sum is bit-identical; the chunk is then folded sequentially in index order.
-// The winner is therefore the reference's plane and `accepted` its exact count.  A candidate
-// identical to the running plane has e == e_cur exactly and is never accepted, so the
-// reference's identity skip (refine.hpp:292) needs no special case.  exp/expf are the glibc
-// ports (glibc_math.cuh).
+// Persistent kernel, one warp per (view, superpixel) task at a time (tasks pulled from a global
+// counter in (superpixel row, view, column) order for L2 locality).  The reference's per-task
+// control flow is a sequential greedy over an ordered candidate list (propagation candidates in
+// grid_neighbors(Kernel) order, then the triangle normals at the current depth) that accepts a
+// candidate iff its energy is strictly above the running best, skipping candidates whose bound
+// E_s (1 + eta) cannot beat it.  The warp reproduces it exactly:
+//   * the candidate list is built in the reference order; E_s of every candidate is computed up
+//     front (8 lanes per candidate); bitwise repeats of earlier planes are marked (they cannot
+//     be accepted) and the task bound m_task <= 1 + eta prunes what the reference's bound prunes
+//     and more, never an acceptable candidate;
+//   * E_c is evaluated lane-per-target (pair_stats, refine.hpp:111-172): each lane walks the
+//     member pixels in the reference's order and keeps photo_sum / vis_sum / x_count in
+//     registers, so every FP64 sum is bit-identical; the per-pixel geometry is computed once per
+//     pixel and broadcast through shared memory; the target's (label, depth, 1/depth) comes from
+//     one gather of the rasterised target (k_build_raster); photo weights are cached per lane;
+//   * with G = 8 or 16 lanes per candidate, 32 / G consecutive surviving candidates are
+//     evaluated at once (speculatively); decisions are still taken in index order with exact
+//     energies, re-testing the later ones after an acceptance.
+// The accepted planes and the accepted count are therefore the reference's.  kFlat selects the
+// rectified / grid-rig specialisations (R = I, t.z = 0, one K).  exp/expf are the glibc ports
+// (glibc_math.cuh).
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>

@@ -1,11 +1,15 @@
 // Plane-sweep initialisation and rasterization on sm_100a.
 //
 //   k_sweep      sweep_view (sweep.hpp:112-139) + sweep_cost (sweep.hpp:85-107): one CTA per
-//                (view, superpixel), one thread per depth hypothesis.  Member rays and reference
-//                colours are staged once in shared memory; each thread accumulates its own FP64
-//                cost in exactly the reference's (target, member-pixel) order, so costs are
-//                bit-identical; the (cost, depth) argmin is a block reduction on a total order,
-//                which reproduces "ties -> smaller depth" (sweep.hpp:130).
+//                (view, superpixel).  Phase A: one thread per depth hypothesis runs the cost
+//                chain over the first target (member rays and colours staged in shared memory);
+//                phase B completes the chain of the best partial hypothesis (its cost B);
+//                phase C continues the others target by target, member-parallel, dropping a
+//                hypothesis as soon as its partial cost exceeds B (exact: partial sums of
+//                non-negative terms never exceed the final sum).  Every chain adds in exactly
+//                the reference's (target, member-pixel) order, so costs are bit-identical; the
+//                (cost, depth) argmin is a block reduction on a total order, which reproduces
+//                "ties -> smaller depth" (sweep.hpp:130).  See the comment above k_sweep.
 //   k_rasterize  rasterize (sweep.hpp:44-63): one thread per pixel.
 //
 // FP64 geometry follows geometry.hpp:70-111 operation by operation.  Two template switches
