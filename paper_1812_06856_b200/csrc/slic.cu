@@ -156,13 +156,44 @@ __global__ void __launch_bounds__(256) k_slic_update(const float4* __restrict__ 
     long long sx = 0, sy = 0;
     int cnt = 0;
     double sc = 0;  // this lane's channel sum (lanes 0-2)
-    for (int y = ya; y < yb; ++y) {
-        for (int xc = xa; xc < xb; xc += 32) {
-            const int x = xc + lane;
-            const bool m = x < xb && lb[(size_t)y * W + x] == id;
+    // (row, 32-wide chunk) steps in row-major order, software-pipelined by one step: the label
+    // and colour of the next step are loaded before the current one is consumed
+    int ny = ya, nx = xa;  // next step to load
+    auto load = [&](int& lv, float4& cv) {
+        const int x = nx + lane;
+        lv = -1;
+        if (x < xb) {
+            const size_t o = (size_t)ny * W + x;
+            lv = lb[o];
+            cv = im[o];
+        }
+        nx += 32;
+        if (nx >= xb) {
+            nx = xa;
+            ++ny;
+        }
+    };
+    int l_next = -1;
+    float4 c_next = make_float4(0.f, 0.f, 0.f, 0.f);
+    const bool any = ya < yb && xa < xb;
+    if (any) load(l_next, c_next);
+    for (int y = ya, xc = xa; any && y < yb;) {
+        const int lv = l_next;
+        const float4 cv = c_next;
+        if (ny < yb) load(l_next, c_next);
+        const int x = xc + lane;
+        xc += 32;
+        const int yc = y;
+        if (xc >= xb) {
+            xc = xa;
+            ++y;
+        }
+        {
+            const int y = yc;
+            const bool m = lv == id;
             unsigned mask = __ballot_sync(LFDG_FULL_MASK, m);
             if (!mask) continue;
-            if (m) buf[lane] = im[(size_t)y * W + x];
+            if (m) buf[lane] = cv;
             const int n = __popc(mask);
             sx += __reduce_add_sync(LFDG_FULL_MASK, m ? (unsigned)x : 0u);
             sy += (long long)y * n;
