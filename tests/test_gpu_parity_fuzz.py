@@ -20,6 +20,10 @@ def _draw(seed):
     grid = [(0, 0), (0, 0), (2, 2), (2, 3)][rng.integers(4)]
     nv = int(rng.integers(2, 6))
     W, H = int(rng.integers(48, 161)), int(rng.integers(40, 121))
+    if rng.random() < 0.2:  # many targets: the 16- and 8-lane group layouts over target rounds
+        grid = [(0, 0), (4, 5), (5, 5), (3, 6)][rng.integers(4)]
+        nv = int(rng.integers(10, 26))
+        W, H = int(rng.integers(40, 81)), int(rng.integers(32, 61))
     rig = ["none", "none", "tz", "rot", "skew", "general"][rng.integers(6)]
     S = int(rng.choice([5, 7, 8, 10, 12, 16]))
     slic = (S, float(rng.choice([0.02, 0.1, 0.4])), int(rng.integers(1, 11)))
