@@ -245,3 +245,17 @@ def test_label_png_reader_all_filter_types(tmp_path):
         _encode_filtered_png(str(p), img, filters)
         back, w, h = art.read_label_png(str(p))
         assert (w, h) == (13, 10) and np.array_equal(back, img.reshape(-1).astype(np.int32)), filters
+
+
+def test_pipeline_config_validation():
+    from paper_1812_06856_b200.api import InvalidParams
+    from paper_1812_06856_b200.run import STAGE_ORDER, PipelineConfig
+
+    assert STAGE_ORDER == ("segment", "init", "refine", "fuse", "eval")  # pipeline.hpp:25-28
+    PipelineConfig(out_dir="x").validate()
+    for bad, match in ((PipelineConfig(), "output directory"), (PipelineConfig(out_dir="x", stages=[]), "no stages"),
+                       (PipelineConfig(out_dir="x", stages=["fuse", "x"]), "unknown stage"),
+                       (PipelineConfig(out_dir="x", dump_every=-1), "bad pipeline"),
+                       (PipelineConfig(out_dir="x", fusion_epsilon=-0.1), "bad pipeline")):
+        with pytest.raises(InvalidParams, match=match):
+            bad.validate()
