@@ -109,3 +109,32 @@ def test_resume_fused_maps_and_missing_products(c1, full_run, tmp_path):
         run_pipeline(c1["lab"], c1["cams"], c1["range"], _cfg(empty, resume=True, stages=["init"]))
     with pytest.raises(api.InvalidParams, match="unknown stage"):
         run_pipeline(c1["lab"], c1["cams"], c1["range"], _cfg(empty, stages=["bogus"]))
+
+
+def test_split_run_artifacts_byte_identical(c1, full_run, tmp_path):
+    """tests/test_pipeline.cpp:139-164: segment+init, then resume refine+fuse(+eval) -> every
+    depth PFM and label PNG byte-identical to the single run."""
+    from paper_1812_06856_b200.run import run_pipeline
+
+    d, _ = full_run
+    run_pipeline(c1["lab"], c1["cams"], c1["range"], _cfg(tmp_path, stages=["segment", "init"]))
+    run_pipeline(c1["lab"], c1["cams"], c1["range"], _cfg(tmp_path, resume=True, stages=["refine", "fuse", "eval"]))
+    for v in range(3):
+        names = ["depth_v%d_stage%d.pfm" % (v, s) for s in (1, 2, 3)] + ["labels_v%d.png" % v,
+                                                                           "planes_v%d_stage2.txt" % v]
+        for name in names:
+            assert (tmp_path / name).read_bytes() == open(os.path.join(str(d), name), "rb").read(), name
+
+
+def test_missing_predecessors_and_corrupt_planes(c1, tmp_path):
+    """tests/test_pipeline.cpp:180-215."""
+    from paper_1812_06856_b200 import api
+    from paper_1812_06856_b200.run import PipelineError, run_pipeline
+
+    with pytest.raises(api.InvalidParams):
+        run_pipeline(c1["lab"], c1["cams"], c1["range"], _cfg(tmp_path / "a", stages=["refine"]))
+    run_pipeline(c1["lab"], c1["cams"], c1["range"], _cfg(tmp_path / "b", stages=["segment", "init"]))
+    (tmp_path / "b" / "planes_v1_stage1.txt").write_text("2\n0x1p+2 0 0 -0x1p+0\n")  # wrong count for the grid
+    with pytest.raises(PipelineError) as e:
+        run_pipeline(c1["lab"], c1["cams"], c1["range"], _cfg(tmp_path / "b", resume=True, stages=["refine"]))
+    assert "init" in str(e.value) and "view 1" in str(e.value)
