@@ -229,6 +229,15 @@ int lfdg_selftest_exp_nonpos(int device, const double* in, double* out, size_t n
 /* Measured FP64 FMA throughput of the device (FLOP/s, DFMA = 2), the sweep/refine roofline. */
 int lfdg_selftest_fp64_peak(int device, double* flops);
 
+/* ---- out-of-bounds-write detector (guard.cu) ------------------------------------------ */
+/* With LFDG_GUARD=1 in the environment every device buffer is bracketed by 64 KiB guard zones
+ * of a fixed byte pattern.  check_guards counts the live buffers and those whose guards were
+ * overwritten (synchronizes the device).  guard_selftest writes one element past a fresh buffer
+ * and sets *detected = 1 when exactly that buffer is reported (LFDG_STATE if guards are off). */
+int lfdg_debug_guard_enabled(void);
+int lfdg_debug_check_guards(uint64_t* n_buffers, uint64_t* n_corrupt);
+int lfdg_debug_guard_selftest(int device, uint64_t* detected);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,7 +66,8 @@ EXPORTED = [
     "lfdg_selftest_exp", "lfdg_selftest_expf", "lfdg_render_scene", "lfdg_rgb_to_scaled_lab",
     "lfdg_upload_images", "lfdg_download_results", "lfdg_selftest_fp64_peak", "lfdg_refine_work", "lfdg_selftest_exp_nonpos",
     "lfdg_fuse_views", "lfdg_get_fused", "lfdg_gather_candidates", "lfdg_stability_fuse", "lfdg_upload_rgb",
-    "lfdg_rgb_to_scaled_lab_gpu", "lfdg_eval_bad_pixel",
+    "lfdg_rgb_to_scaled_lab_gpu", "lfdg_eval_bad_pixel", "lfdg_debug_guard_enabled", "lfdg_debug_check_guards",
+    "lfdg_debug_guard_selftest",
 ]
 
 _lib = None
@@ -154,6 +155,9 @@ def lib():
         "lfdg_get_fused": (I, [P, I, P]),
         "lfdg_gather_candidates": (I, [P, I, P, P, P, C.c_int64, C.POINTER(C.c_int64)]),
         "lfdg_stability_fuse": (I, [I, I, P, P, P, D, P]),
+        "lfdg_debug_guard_enabled": (I, []),
+        "lfdg_debug_check_guards": (I, [PU64, PU64]),
+        "lfdg_debug_guard_selftest": (I, [I, PU64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

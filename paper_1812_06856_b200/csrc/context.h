@@ -43,6 +43,14 @@ struct Error : std::runtime_error {
         (ctx)->launches++;                          \
     } while (0)
 
+// Device allocation with optional guard zones (guard.cu).  With LFDG_GUARD=1 in the environment
+// every buffer gets 64 KiB of a known byte pattern on both sides and an exact-size allocation,
+// and lfdg_debug_check_guards() reports any buffer whose guards were overwritten: an
+// out-of-bounds-write detector for runs where compute-sanitizer is unavailable.
+bool guard_mode();
+void* dev_alloc(size_t bytes);
+void dev_free(void* p);
+
 // Grow-only device buffer: re-allocation (which synchronizes the device) happens only when a
 // larger size is requested, so steady-state calls never allocate.
 template <typename T>
@@ -52,15 +60,15 @@ struct DevBuf {
     size_t cap = 0;  // allocated element count
     void alloc(size_t count) {
         n = count;
-        if (count <= cap && p) return;
-        if (p) cudaFree(p);
+        if (count <= cap && p && !(guard_mode() && count != cap)) return;
+        if (p) dev_free(p);
         p = nullptr;
         cap = 0;
-        if (count) LFDG_CUDA_CHECK(cudaMalloc(&p, count * sizeof(T)));
+        if (count) p = static_cast<T*>(dev_alloc(count * sizeof(T)));
         cap = count;
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) dev_free(p);
         p = nullptr;
         n = cap = 0;
     }
