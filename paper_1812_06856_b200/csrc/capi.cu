@@ -99,6 +99,7 @@ uint64_t lfdg_launch_count(lfdg_ctx* p) { return p ? reinterpret_cast<lfdg::Ctx*
 
 int lfdg_set_views(lfdg_ctx* p, int n_views, int width, int height, const float* images, const lfdg_camera* cameras,
                    double d_min, double d_max) {
+    const lfdg::NvtxRange range_("set_views");
     return guarded([&] {
         auto* c = C(p);
         activate(c);
@@ -151,6 +152,7 @@ int lfdg_update_images(lfdg_ctx* p, int v0, int n, const float* images) {
 }
 
 int lfdg_slic_segment(lfdg_ctx* p, int view, const lfdg_slic_params* params) {
+    const lfdg::NvtxRange range_("slic_segment");
     return guarded([&] {
         auto* c = C(p);
         activate(c);
@@ -161,6 +163,7 @@ int lfdg_slic_segment(lfdg_ctx* p, int view, const lfdg_slic_params* params) {
 }
 
 int lfdg_slic_segment_views(lfdg_ctx* p, int v0, int n, const lfdg_slic_params* params) {
+    const lfdg::NvtxRange range_("slic_segment_views");
     return guarded([&] {
         auto* c = C(p);
         activate(c);
@@ -229,6 +232,7 @@ int lfdg_set_grid(lfdg_ctx* p, int view, int cell_size, const int32_t* label_map
 }
 
 int lfdg_sweep_view(lfdg_ctx* p, int view, const lfdg_sweep_params* params, uint64_t seed, lfdg_plane* planes_out) {
+    const lfdg::NvtxRange range_("sweep_view");
     return guarded([&] {
         auto* c = C(p);
         activate(c);
@@ -244,6 +248,7 @@ int lfdg_sweep_view(lfdg_ctx* p, int view, const lfdg_sweep_params* params, uint
 }
 
 int lfdg_sweep_views(lfdg_ctx* p, int v0, int n, const lfdg_sweep_params* params, uint64_t seed) {
+    const lfdg::NvtxRange range_("sweep_views");
     return guarded([&] {
         auto* c = C(p);
         activate(c);
@@ -287,6 +292,7 @@ int lfdg_get_planes(lfdg_ctx* p, int view, lfdg_plane* planes) {
 }
 
 int lfdg_rasterize(lfdg_ctx* p) {
+    const lfdg::NvtxRange range_("rasterize");
     return guarded([&] {
         auto* c = C(p);
         activate(c);
@@ -296,6 +302,7 @@ int lfdg_rasterize(lfdg_ctx* p) {
 }
 
 int lfdg_rasterize_views(lfdg_ctx* p, int v0, int n) {
+    const lfdg::NvtxRange range_("rasterize_views");
     return guarded([&] {
         auto* c = C(p);
         activate(c);
@@ -327,6 +334,7 @@ int lfdg_set_depth(lfdg_ctx* p, int view, const float* depth) {
 
 int lfdg_make_refine_context(lfdg_ctx* p, const lfdg_energy_params* params, int sweep_levels, double* sigma_out,
                              int* size_init_out) {
+    const lfdg::NvtxRange range_("make_refine_context");
     return guarded([&] {
         auto* c = C(p);
         activate(c);
@@ -348,6 +356,7 @@ int lfdg_set_refine_views(lfdg_ctx* p, int v0, int n) {
 }
 
 int lfdg_refine_iteration(lfdg_ctx* p, int l, uint64_t* accepted, uint64_t* violations) {
+    const lfdg::NvtxRange range_("refine_iteration");
     return guarded([&] {
         auto* c = C(p);
         activate(c);
@@ -366,6 +375,7 @@ int lfdg_refine_iteration(lfdg_ctx* p, int l, uint64_t* accepted, uint64_t* viol
 }
 
 int lfdg_run_refinement(lfdg_ctx* p, uint64_t* accepted, uint64_t* violations) {
+    const lfdg::NvtxRange range_("run_refinement");
     return guarded([&] {
         auto* c = C(p);
         activate(c);
@@ -409,6 +419,7 @@ int lfdg_get_min_nb_sim(lfdg_ctx* p, int view, float* out) {
 }
 
 int lfdg_fuse_views(lfdg_ctx* p, int v0, int n, double epsilon) {
+    const lfdg::NvtxRange range_("fuse_views");
     return guarded([&] {
         auto* c = C(p);
         activate(c);

@@ -21,8 +21,19 @@
 
 #include "../../include/lfdg.h"
 #include "common.cuh"
+#include "nvtx3/nvToolsExt.h"
 
 namespace lfdg {
+
+// NVTX range around a C-ABI stage entry (slic, sweep, rasterize, refine, fuse, transfers), so a
+// profiler timeline groups the kernels by the reference's stage names.  Header-only NVTX v3: a
+// no-op unless a tool is attached.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 struct Error : std::runtime_error {
     int code;

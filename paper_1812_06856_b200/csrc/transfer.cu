@@ -66,6 +66,7 @@ void download_results(Ctx& c, int v0, int n, lfdg_plane* planes, float* depth) {
 extern "C" {
 
 int lfdg_upload_images(lfdg_ctx* p, int v0, int n, const float* images) {
+    const lfdg::NvtxRange range_("upload_images");
     try {
         auto* c = reinterpret_cast<lfdg::Ctx*>(p);
         if (!c) throw lfdg::Error(LFDG_STATE, "null context");
@@ -79,6 +80,7 @@ int lfdg_upload_images(lfdg_ctx* p, int v0, int n, const float* images) {
 }
 
 int lfdg_upload_rgb(lfdg_ctx* p, int v0, int n, const float* rgb) {
+    const lfdg::NvtxRange range_("upload_rgb");
     try {
         auto* c = reinterpret_cast<lfdg::Ctx*>(p);
         if (!c) throw lfdg::Error(LFDG_STATE, "null context");
@@ -113,6 +115,7 @@ int lfdg_rgb_to_scaled_lab_gpu(int device, const float* rgb, float* lab, size_t 
 }
 
 int lfdg_download_results(lfdg_ctx* p, int v0, int n, lfdg_plane* planes, float* depth, int sync) {
+    const lfdg::NvtxRange range_("download_results");
     try {
         auto* c = reinterpret_cast<lfdg::Ctx*>(p);
         if (!c) throw lfdg::Error(LFDG_STATE, "null context");
