@@ -259,3 +259,33 @@ def test_pipeline_config_validation():
                        (PipelineConfig(out_dir="x", fusion_epsilon=-0.1), "bad pipeline")):
         with pytest.raises(InvalidParams, match=match):
             bad.validate()
+
+
+def test_hexfloat_matches_libstdcxx_ostream(tmp_path):
+    """The reference writes planes with ``f << std::hexfloat << value`` (pipeline.hpp:150-152):
+    compile exactly that with g++ and compare its bytes with artifacts.hexfloat, and read the
+    libstdc++ output back through read_planes."""
+    import shutil
+    import subprocess
+
+    if shutil.which("g++") is None:
+        pytest.skip("g++ not available")
+    src = tmp_path / "hexf.cpp"
+    src.write_text(
+        "#include <cstdio>\n#include <iostream>\n#include <sstream>\n#include <vector>\n"
+        "int main(){ std::vector<double> v; double x; while (std::fread(&x, 8, 1, stdin) == 1) v.push_back(x);\n"
+        "  std::cout << v.size() / 4 << \"\\n\"; std::cout << std::hexfloat;\n"
+        "  for (size_t i = 0; i + 3 < v.size(); i += 4)\n"
+        "    std::cout << v[i] << \" \" << v[i+1] << \" \" << v[i+2] << \" \" << v[i+3] << \"\\n\";\n"
+        "  return 0; }\n")
+    exe = tmp_path / "hexf"
+    subprocess.run(["g++", "-O1", "-o", str(exe), str(src)], check=True)
+    rng = np.random.default_rng(13)
+    vals = np.array(_doubles(rng, 400)[:4 * 200], np.float64)
+    vals = vals[: len(vals) // 4 * 4]
+    out = subprocess.run([str(exe)], input=vals.tobytes(), capture_output=True, check=True).stdout.decode()
+    p = tmp_path / "planes.txt"
+    art.write_planes(vals.reshape(-1, 4), str(p))
+    assert p.read_text() == out
+    p.write_text(out)
+    assert art.read_planes(str(p)).tobytes() == vals.tobytes()
