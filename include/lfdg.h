@@ -148,6 +148,10 @@ int lfdg_upload_images(lfdg_ctx* ctx, int v0, int n, const float* images);
  * conversion to scaled LAB on the device: rgb_to_scaled_lab (image.hpp:97-107), bit-identical to
  * the reference (glibc powf / cbrtf ports), replacing the host pre-pass of pipeline.hpp:245. */
 int lfdg_upload_rgb(lfdg_ctx* ctx, int v0, int n, const float* rgb);
+/* The same from 8-bit sRGB [n][H][W][3] bytes in R, G, B order (a decoded image): each channel
+ * becomes byte / 255.f as read_image does (io.hpp:136-146), then rgb_to_scaled_lab; a quarter of
+ * the host->device bytes of lfdg_upload_rgb. */
+int lfdg_upload_rgb8(lfdg_ctx* ctx, int v0, int n, const unsigned char* rgb8);
 /* Enqueue the download of planes [n][nsp] and depth [n][H][W] of views [v0, v0+n) (either may be
  * NULL); sync != 0 waits for completion. */
 int lfdg_download_results(lfdg_ctx* ctx, int v0, int n, lfdg_plane* planes, float* depth, int sync);
@@ -190,7 +194,8 @@ int lfdg_stability_fuse(int device, int n_pixels, const int32_t* offsets, const 
 /* Raw device pointer + byte size of one all-view buffer, laid out [V][per-view block]:
  * 0 labels i32[H*W], 1 centroid x f64[nsp], 2 centroid y f64[nsp], 3 mean colour f32x4[nsp],
  * 4 pixel count i32[nsp], 5 member offsets i32[nsp+1], 6 member pixels i32[H*W],
- * 7 planes f64x4[nsp], 8 depth f32[H*W], 9 centroid rays f64x2[nsp].  *view_stride is the
+ * 7 planes f64x4[nsp], 8 depth f32[H*W], 9 centroid rays f64x2[nsp], 10 scaled LAB f32x4[H*W]
+ * (L, a, b, 0).  *view_stride is the
  * per-view block size in bytes. */
 int lfdg_device_buffer(lfdg_ctx* ctx, int which, void** ptr, size_t* bytes, size_t* view_stride);
 /* After an external all-gather filled buffers of views this context did not compute. */

@@ -20,7 +20,7 @@ LFDG_CUDA = 3
 LFDG_STATE = 4
 
 # Buffer ids of lfdg_device_buffer.
-BUF_LABELS, BUF_CX, BUF_CY, BUF_COLOR, BUF_COUNT, BUF_MOFF, BUF_MPIX, BUF_PLANES, BUF_DEPTH, BUF_CRAY = range(10)
+BUF_LABELS, BUF_CX, BUF_CY, BUF_COLOR, BUF_COUNT, BUF_MOFF, BUF_MPIX, BUF_PLANES, BUF_DEPTH, BUF_CRAY, BUF_LAB = range(11)
 
 
 class Camera(C.Structure):
@@ -67,7 +67,7 @@ EXPORTED = [
     "lfdg_upload_images", "lfdg_download_results", "lfdg_selftest_fp64_peak", "lfdg_refine_work", "lfdg_selftest_exp_nonpos",
     "lfdg_fuse_views", "lfdg_get_fused", "lfdg_gather_candidates", "lfdg_stability_fuse", "lfdg_upload_rgb",
     "lfdg_rgb_to_scaled_lab_gpu", "lfdg_eval_bad_pixel", "lfdg_debug_guard_enabled", "lfdg_debug_check_guards",
-    "lfdg_debug_guard_selftest",
+    "lfdg_debug_guard_selftest", "lfdg_upload_rgb8",
 ]
 
 _lib = None
@@ -155,6 +155,7 @@ def lib():
         "lfdg_get_fused": (I, [P, I, P]),
         "lfdg_gather_candidates": (I, [P, I, P, P, P, C.c_int64, C.POINTER(C.c_int64)]),
         "lfdg_stability_fuse": (I, [I, I, P, P, P, D, P]),
+        "lfdg_upload_rgb8": (I, [P, I, I, P]),
         "lfdg_debug_guard_enabled": (I, []),
         "lfdg_debug_check_guards": (I, [PU64, PU64]),
         "lfdg_debug_guard_selftest": (I, [I, PU64]),

@@ -179,6 +179,13 @@ class DeviceContext:
         N.check(self.L.lfdg_upload_rgb(self.h, v0, rgb.shape[0], N.ptr(rgb)))
         self.synchronize()
 
+    def upload_rgb8(self, rgb8: np.ndarray, v0: int = 0):
+        """Replace the LAB images of views [v0, v0 + n) by rgb_to_scaled_lab of the 8-bit sRGB images
+        rgb8 [n][H][W][3] (R, G, B bytes; each channel / 255.f as read_image, io.hpp:136-146)."""
+        rgb8 = np.ascontiguousarray(rgb8, np.uint8)
+        N.check(self.L.lfdg_upload_rgb8(self.h, v0, rgb8.shape[0], N.ptr(rgb8)))
+        self.synchronize()
+
     def launch_count(self) -> int:
         return int(self.L.lfdg_launch_count(self.h))
 

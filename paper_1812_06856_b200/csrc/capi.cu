@@ -473,6 +473,7 @@ int lfdg_device_buffer(lfdg_ctx* p, int which, void** ptr, size_t* bytes, size_t
             case 7: q = c->planes.p; stride = nsp * 32; break;
             case 8: q = c->depth.p; stride = hw * 4; break;
             case 9: q = c->cray.p; stride = nsp * 16; break;
+            case 10: q = c->lab.p; stride = hw * 16; break;
             default: throw lfdg::Error(LFDG_STATE, "unknown buffer id");
         }
         if (!q) throw lfdg::Error(LFDG_STATE, "buffer not allocated yet");

@@ -122,7 +122,8 @@ struct FuseScratch {
     DevBuf<long long> ckey;
 };
 struct StagingScratch {
-    DevBuf<float> buf;  // [V][H*W*3] upload staging
+    DevBuf<float> buf;           // [V][H*W*3] upload staging
+    DevBuf<unsigned char> buf8;  // [V][H*W*3] 8-bit sRGB upload staging
 };
 
 struct Ctx {
@@ -193,6 +194,7 @@ std::vector<int> matching_views(const Ctx& c, int view, int max_neighbors);    /
 void make_refine_tables(Ctx& c, const lfdg_energy_params& p, int sweep_levels);  // refine.cu
 void refine_iteration(Ctx& c, int l);                                            // refine.cu
 void upload_images(Ctx& c, int v0, int n, const float* host);                     // transfer.cu
+void upload_rgb8(Ctx& c, int v0, int n, const unsigned char* host);              // transfer.cu
 void fuse_views(Ctx& c, int v0, int n, double eps);                                // fusion.cu
 long long gather_candidates_host(Ctx& c, int ref, int32_t* offsets, float* depths, int32_t* views,
                                  long long capacity);                              // fusion.cu

@@ -20,7 +20,33 @@ __global__ void k_rgb_to_lab(const float* __restrict__ src, float4* __restrict__
     libm::rgb_to_scaled_lab(src[3 * i], src[3 * i + 1], src[3 * i + 2], L, A, B);
     dst[i] = make_float4(L, A, B, 0.f);
 }
+// 8-bit sRGB (read_image, io.hpp:136-146: channel / 255.f) -> rgb_to_scaled_lab -> float4, so
+// decoded 8-bit views cross PCIe at a quarter of the float bytes.
+__global__ void k_rgb8_to_lab(const unsigned char* __restrict__ src, float4* __restrict__ dst, size_t n) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float r = (float)src[3 * i] / 255.f, g = (float)src[3 * i + 1] / 255.f, b = (float)src[3 * i + 2] / 255.f;
+    float L, A, B;
+    libm::rgb_to_scaled_lab(r, g, b, L, A, B);
+    dst[i] = make_float4(L, A, B, 0.f);
+}
 }  // namespace
+
+// 8-bit sRGB images in ([n][H][W][3] bytes, R G B order), converted like read_image +
+// rgb_to_scaled_lab on the device.
+void upload_rgb8(Ctx& c, int v0, int n, const unsigned char* host) {
+    c.require_views();
+    if (v0 < 0 || n < 0 || v0 + n > c.V) throw Error(LFDG_STATE, "view range out of bounds");
+    if (n == 0) return;
+    if (!host) throw Error(LFDG_STATE, "null images");
+    const size_t hw = c.hw();
+    StagingScratch& s = c.stage_s;
+    s.buf8.alloc((size_t)c.V * hw * 3);
+    LFDG_CUDA_CHECK(cudaMemcpyAsync(s.buf8.p, host, (size_t)n * hw * 3, cudaMemcpyHostToDevice, c.stream));
+    const size_t m = (size_t)n * hw;
+    k_rgb8_to_lab<<<(unsigned)((m + 255) / 256), 256, 0, c.stream>>>(s.buf8.p, c.lab.p + (size_t)v0 * hw, m);
+    LFDG_LAUNCHED(&c);
+}
 
 // sRGB images in ([n][H][W][3] floats in [0, 1]), converted to the scaled LAB the hot path reads
 // on the device (the reference converts on the host before the path, pipeline.hpp:245).
@@ -86,6 +112,20 @@ int lfdg_upload_rgb(lfdg_ctx* p, int v0, int n, const float* rgb) {
         if (!c) throw lfdg::Error(LFDG_STATE, "null context");
         LFDG_CUDA_CHECK(cudaSetDevice(c->device));
         lfdg::upload_rgb(*c, v0, n, rgb);
+        return LFDG_OK;
+    } catch (const lfdg::Error& e) {
+        lfdg::set_last_error(e.what());
+        return e.code;
+    }
+}
+
+int lfdg_upload_rgb8(lfdg_ctx* p, int v0, int n, const unsigned char* rgb8) {
+    const lfdg::NvtxRange range_("upload_rgb8");
+    try {
+        auto* c = reinterpret_cast<lfdg::Ctx*>(p);
+        if (!c) throw lfdg::Error(LFDG_STATE, "null context");
+        LFDG_CUDA_CHECK(cudaSetDevice(c->device));
+        lfdg::upload_rgb8(*c, v0, n, rgb8);
         return LFDG_OK;
     } catch (const lfdg::Error& e) {
         lfdg::set_last_error(e.what());

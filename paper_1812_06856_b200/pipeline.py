@@ -148,6 +148,12 @@ class HotPath:
         rgb_host = np.ascontiguousarray(rgb_host, np.float32)
         N.check(N.lib().lfdg_upload_rgb(self.ctx.h, 0, self.V, N.ptr(rgb_host)))
 
+    def upload_rgb8(self, rgb8_host: np.ndarray):
+        """Enqueue the H2D copy of every view's 8-bit sRGB image (a decoded image file, 1 B per
+        channel) and its conversion to scaled LAB on the device (read_image + rgb_to_scaled_lab)."""
+        rgb8_host = np.ascontiguousarray(rgb8_host, np.uint8)
+        N.check(N.lib().lfdg_upload_rgb8(self.ctx.h, 0, self.V, N.ptr(rgb8_host)))
+
     def download(self, planes_host: Optional[np.ndarray], depth_host: Optional[np.ndarray], sync: bool = True):
         """Enqueue the D2H copy of this rank's views' planes [n][nsp][4] and depth [n][H][W]."""
         N.check(N.lib().lfdg_download_results(self.ctx.h, self.v0, self.n,
