@@ -152,6 +152,21 @@ int lfdg_upload_rgb(lfdg_ctx* ctx, int v0, int n, const float* rgb);
  * becomes byte / 255.f as read_image does (io.hpp:136-146), then rgb_to_scaled_lab; a quarter of
  * the host->device bytes of lfdg_upload_rgb. */
 int lfdg_upload_rgb8(lfdg_ctx* ctx, int v0, int n, const unsigned char* rgb8);
+/* Pipelined transfers for streaming many view sets through one context (a copy stream next to
+ * the compute stream):
+ *   prefetch_images   H2D of views [v0, v0+n) (scaled-LAB floats, pinned) into the staging
+ *                     buffer on the copy stream, once the previous commit has consumed it;
+ *   commit_images     on the compute stream: wait for that copy, install it as the views' LAB;
+ *   download_results_async  D2H of planes / depth (as lfdg_download_results) on the copy stream,
+ *                     after the compute work enqueued so far;
+ *   wait_downloads    the compute stream waits for the last async download (call before the
+ *                     next sweep overwrites planes / depth).
+ * Step k's download and step k+1's upload then overlap the compute of steps k+1 / k.
+ * lfdg_synchronize waits for both streams. */
+int lfdg_prefetch_images(lfdg_ctx* ctx, int v0, int n, const float* images);
+int lfdg_commit_images(lfdg_ctx* ctx);
+int lfdg_download_results_async(lfdg_ctx* ctx, int v0, int n, lfdg_plane* planes, float* depth);
+int lfdg_wait_downloads(lfdg_ctx* ctx);
 /* Enqueue the download of planes [n][nsp] and depth [n][H][W] of views [v0, v0+n) (either may be
  * NULL); sync != 0 waits for completion. */
 int lfdg_download_results(lfdg_ctx* ctx, int v0, int n, lfdg_plane* planes, float* depth, int sync);

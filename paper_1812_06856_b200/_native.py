@@ -67,7 +67,8 @@ EXPORTED = [
     "lfdg_upload_images", "lfdg_download_results", "lfdg_selftest_fp64_peak", "lfdg_refine_work", "lfdg_selftest_exp_nonpos",
     "lfdg_fuse_views", "lfdg_get_fused", "lfdg_gather_candidates", "lfdg_stability_fuse", "lfdg_upload_rgb",
     "lfdg_rgb_to_scaled_lab_gpu", "lfdg_eval_bad_pixel", "lfdg_debug_guard_enabled", "lfdg_debug_check_guards",
-    "lfdg_debug_guard_selftest", "lfdg_upload_rgb8",
+    "lfdg_debug_guard_selftest", "lfdg_upload_rgb8", "lfdg_prefetch_images", "lfdg_commit_images",
+    "lfdg_download_results_async", "lfdg_wait_downloads",
 ]
 
 _lib = None
@@ -156,6 +157,10 @@ def lib():
         "lfdg_gather_candidates": (I, [P, I, P, P, P, C.c_int64, C.POINTER(C.c_int64)]),
         "lfdg_stability_fuse": (I, [I, I, P, P, P, D, P]),
         "lfdg_upload_rgb8": (I, [P, I, I, P]),
+        "lfdg_prefetch_images": (I, [P, I, I, P]),
+        "lfdg_commit_images": (I, [P]),
+        "lfdg_download_results_async": (I, [P, I, I, P, P]),
+        "lfdg_wait_downloads": (I, [P]),
         "lfdg_debug_guard_enabled": (I, []),
         "lfdg_debug_check_guards": (I, [PU64, PU64]),
         "lfdg_debug_guard_selftest": (I, [I, PU64]),

@@ -76,6 +76,8 @@ void lfdg_destroy(lfdg_ctx* p) {
     auto* c = reinterpret_cast<lfdg::Ctx*>(p);
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
+    if (c->pipe.stream) cudaStreamSynchronize(c->pipe.stream);
+    c->pipe.destroy();
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
 }
@@ -92,6 +94,7 @@ int lfdg_synchronize(lfdg_ctx* p) {
         auto* c = C(p);
         activate(c);
         LFDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        if (c->pipe.stream) LFDG_CUDA_CHECK(cudaStreamSynchronize(c->pipe.stream));
     });
 }
 

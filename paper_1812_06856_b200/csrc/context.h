@@ -126,10 +126,25 @@ struct StagingScratch {
     DevBuf<unsigned char> buf8;  // [V][H*W*3] 8-bit sRGB upload staging
 };
 
+// Pipelined transfers (transfer.cu): a copy stream moves the next step's views into the staging
+// buffer and the previous step's results out while the compute stream works.
+struct CopyPipe {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t staged = nullptr, consumed = nullptr, computed = nullptr, downloaded = nullptr;
+    int v0 = 0, n = 0;
+    bool has_staged = false, has_download = false;
+    void destroy() {
+        for (cudaEvent_t* e : {&staged, &consumed, &computed, &downloaded})
+            if (*e) cudaEventDestroy(*e), *e = nullptr;
+        if (stream) cudaStreamDestroy(stream), stream = nullptr;
+    }
+};
+
 struct Ctx {
     int device = 0;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
+    CopyPipe pipe;
     uint64_t launches = 0;
     int sm_count = 148;
 
@@ -195,6 +210,10 @@ void make_refine_tables(Ctx& c, const lfdg_energy_params& p, int sweep_levels); 
 void refine_iteration(Ctx& c, int l);                                            // refine.cu
 void upload_images(Ctx& c, int v0, int n, const float* host);                     // transfer.cu
 void upload_rgb8(Ctx& c, int v0, int n, const unsigned char* host);              // transfer.cu
+void prefetch_images(Ctx& c, int v0, int n, const float* host);                  // transfer.cu
+void commit_images(Ctx& c);                                                       // transfer.cu
+void download_results_async(Ctx& c, int v0, int n, lfdg_plane* planes, float* depth);  // transfer.cu
+void wait_downloads(Ctx& c);                                                      // transfer.cu
 void fuse_views(Ctx& c, int v0, int n, double eps);                                // fusion.cu
 long long gather_candidates_host(Ctx& c, int ref, int32_t* offsets, float* depths, int32_t* views,
                                  long long capacity);                              // fusion.cu

@@ -76,6 +76,76 @@ void upload_images(Ctx& c, int v0, int n, const float* host) {
     LFDG_LAUNCHED(&c);
 }
 
+// ---- pipelined transfers ---------------------------------------------------------------------
+static void ensure_pipe(Ctx& c) {
+    CopyPipe& q = c.pipe;
+    if (q.stream) return;
+    LFDG_CUDA_CHECK(cudaStreamCreateWithFlags(&q.stream, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&q.staged, &q.consumed, &q.computed, &q.downloaded})
+        LFDG_CUDA_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    LFDG_CUDA_CHECK(cudaEventRecord(q.consumed, c.stream));  // the staging buffer starts free
+}
+
+// H2D of views [v0, v0+n) (scaled LAB floats) into the staging buffer on the copy stream, after
+// the previous commit has consumed it; overlaps whatever the compute stream is doing.
+void prefetch_images(Ctx& c, int v0, int n, const float* host) {
+    c.require_views();
+    if (v0 < 0 || n < 1 || v0 + n > c.V) throw Error(LFDG_STATE, "view range out of bounds");
+    if (!host) throw Error(LFDG_STATE, "null images");
+    ensure_pipe(c);
+    CopyPipe& q = c.pipe;
+    if (q.has_staged) throw Error(LFDG_STATE, "a prefetched upload is still uncommitted");
+    const size_t hw = c.hw();
+    c.stage_s.buf.alloc((size_t)c.V * hw * 3);
+    LFDG_CUDA_CHECK(cudaStreamWaitEvent(q.stream, q.consumed, 0));
+    LFDG_CUDA_CHECK(cudaMemcpyAsync(c.stage_s.buf.p, host, (size_t)n * hw * 3 * sizeof(float), cudaMemcpyHostToDevice,
+                                    q.stream));
+    LFDG_CUDA_CHECK(cudaEventRecord(q.staged, q.stream));
+    q.v0 = v0;
+    q.n = n;
+    q.has_staged = true;
+}
+
+// On the compute stream: wait for the staged copy and repack it into the LAB the kernels read.
+void commit_images(Ctx& c) {
+    CopyPipe& q = c.pipe;
+    if (!q.has_staged) throw Error(LFDG_STATE, "no prefetched upload to commit");
+    const size_t hw = c.hw();
+    LFDG_CUDA_CHECK(cudaStreamWaitEvent(c.stream, q.staged, 0));
+    const size_t m = (size_t)q.n * hw;
+    k_repack<<<(unsigned)((m + 255) / 256), 256, 0, c.stream>>>(c.stage_s.buf.p, c.lab.p + (size_t)q.v0 * hw, m);
+    LFDG_LAUNCHED(&c);
+    LFDG_CUDA_CHECK(cudaEventRecord(q.consumed, c.stream));
+    q.has_staged = false;
+}
+
+// D2H of the current planes / depth of views [v0, v0+n) on the copy stream, ordered after the
+// work enqueued so far on the compute stream.  Call wait_downloads before anything overwrites
+// planes or depth (the next sweep).
+void download_results_async(Ctx& c, int v0, int n, lfdg_plane* planes, float* depth) {
+    c.require_views();
+    if (v0 < 0 || n < 0 || v0 + n > c.V) throw Error(LFDG_STATE, "view range out of bounds");
+    ensure_pipe(c);
+    CopyPipe& q = c.pipe;
+    LFDG_CUDA_CHECK(cudaEventRecord(q.computed, c.stream));
+    LFDG_CUDA_CHECK(cudaStreamWaitEvent(q.stream, q.computed, 0));
+    if (planes)
+        LFDG_CUDA_CHECK(cudaMemcpyAsync(planes, c.planes.p + (size_t)v0 * c.nsp, (size_t)n * c.nsp * sizeof(lfdg_plane),
+                                        cudaMemcpyDeviceToHost, q.stream));
+    if (depth)
+        LFDG_CUDA_CHECK(cudaMemcpyAsync(depth, c.depth.p + (size_t)v0 * c.hw(), (size_t)n * c.hw() * sizeof(float),
+                                        cudaMemcpyDeviceToHost, q.stream));
+    LFDG_CUDA_CHECK(cudaEventRecord(q.downloaded, q.stream));
+    q.has_download = true;
+}
+
+void wait_downloads(Ctx& c) {
+    CopyPipe& q = c.pipe;
+    if (!q.has_download) return;
+    LFDG_CUDA_CHECK(cudaStreamWaitEvent(c.stream, q.downloaded, 0));
+    q.has_download = false;
+}
+
 void download_results(Ctx& c, int v0, int n, lfdg_plane* planes, float* depth) {
     c.require_views();
     if (v0 < 0 || n < 0 || v0 + n > c.V) throw Error(LFDG_STATE, "view range out of bounds");
@@ -118,6 +188,35 @@ int lfdg_upload_rgb(lfdg_ctx* p, int v0, int n, const float* rgb) {
         return e.code;
     }
 }
+
+#define LFDG_TRANSFER_ENTRY(body)                                   \
+    try {                                                           \
+        auto* c = reinterpret_cast<lfdg::Ctx*>(p);                  \
+        if (!c) throw lfdg::Error(LFDG_STATE, "null context");     \
+        LFDG_CUDA_CHECK(cudaSetDevice(c->device));                  \
+        body;                                                       \
+        return LFDG_OK;                                             \
+    } catch (const lfdg::Error& e) {                                \
+        lfdg::set_last_error(e.what());                             \
+        return e.code;                                              \
+    }
+
+int lfdg_prefetch_images(lfdg_ctx* p, int v0, int n, const float* images) {
+    const lfdg::NvtxRange range_("prefetch_images");
+    LFDG_TRANSFER_ENTRY(lfdg::prefetch_images(*c, v0, n, images))
+}
+
+int lfdg_commit_images(lfdg_ctx* p) {
+    const lfdg::NvtxRange range_("commit_images");
+    LFDG_TRANSFER_ENTRY(lfdg::commit_images(*c))
+}
+
+int lfdg_download_results_async(lfdg_ctx* p, int v0, int n, lfdg_plane* planes, float* depth) {
+    const lfdg::NvtxRange range_("download_results_async");
+    LFDG_TRANSFER_ENTRY(lfdg::download_results_async(*c, v0, n, planes, depth))
+}
+
+int lfdg_wait_downloads(lfdg_ctx* p) { LFDG_TRANSFER_ENTRY(lfdg::wait_downloads(*c)) }
 
 int lfdg_upload_rgb8(lfdg_ctx* p, int v0, int n, const unsigned char* rgb8) {
     const lfdg::NvtxRange range_("upload_rgb8");

@@ -122,6 +122,7 @@ class HotPath:
         c, cfg = self.ctx, self.cfg
         c.slic_views(self.v0, self.n, cfg.slic)
         self._exchange_grids()
+        N.check(N.lib().lfdg_wait_downloads(c.h))  # a pending async download still reads planes / depth
         c.sweep_views(self.v0, self.n, cfg.sweep, cfg.seed)
         self._exchange_planes()
         c.rasterize()
@@ -147,6 +148,26 @@ class HotPath:
         device (rgb_to_scaled_lab, image.hpp:97-107; the reference does it on the host)."""
         rgb_host = np.ascontiguousarray(rgb_host, np.float32)
         N.check(N.lib().lfdg_upload_rgb(self.ctx.h, 0, self.V, N.ptr(rgb_host)))
+
+    # ---- pipelined end-to-end transfers (copy stream next to the compute stream)
+    def prefetch(self, images_host: np.ndarray):
+        """Enqueue the H2D copy of every view's LAB image into the staging buffer on the copy
+        stream; it overlaps the compute already enqueued.  Install it with commit()."""
+        images_host = np.ascontiguousarray(images_host, np.float32)
+        N.check(N.lib().lfdg_prefetch_images(self.ctx.h, 0, self.V, N.ptr(images_host)))
+
+    def commit(self):
+        N.check(N.lib().lfdg_commit_images(self.ctx.h))
+
+    def download_async(self, planes_host: Optional[np.ndarray], depth_host: Optional[np.ndarray]):
+        """D2H of this rank's planes / depth on the copy stream, overlapping the next step's SLIC
+        (run() makes the next sweep wait for it)."""
+        N.check(N.lib().lfdg_download_results_async(self.ctx.h, self.v0, self.n,
+                                                    None if planes_host is None else N.ptr(planes_host),
+                                                    None if depth_host is None else N.ptr(depth_host)))
+
+    def wait_downloads(self):
+        N.check(N.lib().lfdg_wait_downloads(self.ctx.h))
 
     def upload_rgb8(self, rgb8_host: np.ndarray):
         """Enqueue the H2D copy of every view's 8-bit sRGB image (a decoded image file, 1 B per
