@@ -10,8 +10,11 @@ the reference fixtures (byte-identical, tests/test_scene.py).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
 
-Multi-GPU: launched under torchrun; views are partitioned across ranks (strong scaling of the
-fixed view set) with NCCL exchanges (paper_1812_06856_b200/pipeline.py).
+Multi-GPU: under torchrun (or `python bench.py --gpus N`, which starts the N ranks itself through
+torch.distributed.run); views are partitioned across ranks (strong scaling of the fixed view
+set) with NCCL exchanges (paper_1812_06856_b200/pipeline.py).  The default workload stays C3 at
+every N, so the N=1 line of a scaling run equals the single-GPU bench; `--config C5` (64 views,
+8 nearest matching views) is the view-scaling workload of BASELINE configs[4].
 
 `--impl reference` times the reference's own CPU implementation (oracle/_ref: the unmodified
 reference headers) on the host cores, on a bounded sample of the same workload per step
@@ -430,14 +433,30 @@ def cpu_baseline(cfg_name: str) -> dict:
         return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
 
 
+def free_port() -> int:
+    import socket
+
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        run_reference(args, rank, world)
+        run_reference(args, rank, world)  # rank 0 alone runs the host-CPU reference
         return
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # `python bench.py --gpus N` without a launcher: start the N ranks (one process per GPU)
+        # through torch.distributed.run, exactly as the driver's torchrun launch does.
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.run(cmd).returncode)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU")
     if world > 1:
         import torch
         import torch.distributed as dist

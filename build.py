@@ -36,11 +36,29 @@ def _stale(target: str, sources) -> bool:
 
 
 def build_product(force: bool = False, verbose: bool = False) -> str:
+    """One nvcc per translation unit (in parallel, objects under build/), then one link."""
+    from concurrent.futures import ThreadPoolExecutor
+
     sources = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
-    deps = sources + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + [
+    headers = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + [
         os.path.join(ROOT, "include", "lfdg.h")]
-    if force or _stale(LIB, deps):
-        cmd = ["nvcc", *NVCC_FLAGS, *sources, "-o", LIB]
+    odir = os.path.join(ROOT, "build")
+    os.makedirs(odir, exist_ok=True)
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+
+    def obj(src):
+        o = os.path.join(odir, os.path.basename(src) + ".o")
+        if force or _stale(o, [src] + headers):
+            cmd = ["nvcc", *compile_flags, "-c", src, "-o", o]
+            if verbose:
+                print(" ".join(cmd), flush=True)
+            subprocess.run(cmd, check=True, cwd=ROOT)
+        return o
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(sources), os.cpu_count() or 1))) as ex:
+        objs = list(ex.map(obj, sources))
+    if force or _stale(LIB, objs):
+        cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *objs, "-o", LIB]
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True, cwd=ROOT)

@@ -34,6 +34,14 @@ class SlicParams:  # superpixel.hpp:18
     compactness: float = 0.10
     iterations: int = 10
 
+    def validate(self) -> None:  # superpixel.hpp:23-27
+        if self.size < 4:
+            raise InvalidParams("superpixel size must be >= 4")
+        if self.compactness <= 0:
+            raise InvalidParams("compactness must be > 0")
+        if self.iterations < 1:
+            raise InvalidParams("iterations must be >= 1")
+
     def c(self):
         return N.SlicParamsC(self.size, self.compactness, self.iterations)
 
@@ -43,6 +51,12 @@ class SweepParams:  # sweep.hpp:14
     levels: int = 80
     tssd_threshold: float = 0.05
     max_neighbors: int = 0
+
+    def validate(self) -> None:  # sweep.hpp:19-22
+        if self.levels < 2:
+            raise InvalidParams("sweep levels must be >= 2")
+        if self.tssd_threshold <= 0:
+            raise InvalidParams("tssd threshold must be > 0")
 
     def c(self):
         return N.SweepParamsC(self.levels, self.tssd_threshold, self.max_neighbors)
@@ -60,6 +74,12 @@ class EnergyParams:  # refine.hpp:15
     use_smoothness: bool = True
     use_consistency: bool = True
     use_occlusion: bool = True
+
+    def validate(self) -> None:  # refine.hpp:28-31
+        if self.sigma < 0 or self.alpha <= 0 or self.eta < 0 or self.eta > 1:
+            raise InvalidParams("bad energy params")
+        if self.steps_init <= 0 or self.size_init < 0 or self.iterations < 0:
+            raise InvalidParams("bad kernel params")
 
     def c(self):
         return N.EnergyParamsC(self.sigma, self.alpha, self.eta, self.size_init, self.steps_init, self.iterations,
@@ -140,6 +160,27 @@ class RefineStats:  # refine.hpp:244
     violations: int = 0
 
 
+# ----------------------------------------------------------------------------- shape checks
+# The C-ABI takes raw pointers and derives every size from (V, W, H) of the context, so a wrongly
+# shaped array would be over-read on the host (or by an async DMA).  Check before the call and
+# raise InvalidParams like the reference's validation does.
+
+
+def check_images(images: np.ndarray, what: str = "images", H: Optional[int] = None, W: Optional[int] = None,
+                 n_max: Optional[int] = None) -> None:
+    if images.ndim != 4 or images.shape[3] != 3 or images.shape[0] < 1:
+        raise InvalidParams(f"{what} must be [n][H][W][3], got shape {tuple(images.shape)}")
+    if H is not None and (images.shape[1], images.shape[2]) != (H, W):
+        raise InvalidParams(f"{what} are {images.shape[2]}x{images.shape[1]}, the context holds {W}x{H} views")
+    if n_max is not None and images.shape[0] > n_max:
+        raise InvalidParams(f"{what}: {images.shape[0]} views, at most {n_max} fit")
+
+
+def check_shape(a: np.ndarray, shape: tuple, what: str) -> None:
+    if tuple(a.shape) != tuple(shape):
+        raise InvalidParams(f"{what} must have shape {tuple(shape)}, got {tuple(a.shape)}")
+
+
 # ----------------------------------------------------------------------------- device context
 
 
@@ -176,6 +217,7 @@ class DeviceContext:
         """Replace the LAB images of views [v0, v0 + n) by rgb_to_scaled_lab (image.hpp:97-107) of the
         sRGB images rgb [n][H][W][3], converted on the device (bit-identical to the reference)."""
         rgb = np.ascontiguousarray(rgb, np.float32)
+        check_images(rgb, "rgb images", self.H, self.W, self.V - v0)
         N.check(self.L.lfdg_upload_rgb(self.h, v0, rgb.shape[0], N.ptr(rgb)))
         self.synchronize()
 
@@ -183,6 +225,7 @@ class DeviceContext:
         """Replace the LAB images of views [v0, v0 + n) by rgb_to_scaled_lab of the 8-bit sRGB images
         rgb8 [n][H][W][3] (R, G, B bytes; each channel / 255.f as read_image, io.hpp:136-146)."""
         rgb8 = np.ascontiguousarray(rgb8, np.uint8)
+        check_images(rgb8, "rgb8 images", self.H, self.W, self.V - v0)
         N.check(self.L.lfdg_upload_rgb8(self.h, v0, rgb8.shape[0], N.ptr(rgb8)))
         self.synchronize()
 
@@ -200,14 +243,21 @@ class DeviceContext:
     # -- views
     def set_views(self, images: np.ndarray, cams: np.ndarray, d_range: Sequence[float]):
         images = np.ascontiguousarray(images, np.float32)
-        cams = np.ascontiguousarray(cams, np.float64).reshape(-1, 21)
+        check_images(images)
+        cams = np.ascontiguousarray(cams, np.float64)
         V, H, W = images.shape[:3]
+        if cams.size != V * 21:
+            raise InvalidParams(f"cameras must be [{V}][21] (K, R row-major, t), got shape {tuple(cams.shape)}")
+        cams = cams.reshape(V, 21)
+        if len(d_range) != 2:
+            raise InvalidParams("depth range must be (d_min, d_max)")
         N.check(self.L.lfdg_set_views(self.h, V, W, H, N.ptr(images), N.ptr(cams), float(d_range[0]),
                                       float(d_range[1])))
         self.V, self.W, self.H = V, W, H
 
     def update_images(self, v0: int, images: np.ndarray):
         images = np.ascontiguousarray(images, np.float32)
+        check_images(images, "images", self.H, self.W, self.V - v0)
         N.check(self.L.lfdg_update_images(self.h, v0, images.shape[0], N.ptr(images)))
 
     # -- SLIC
@@ -236,6 +286,8 @@ class DeviceContext:
 
     def set_grid(self, view: int, cell_size: int, label_map: np.ndarray):
         lm = np.ascontiguousarray(label_map, np.int32).reshape(-1)
+        if lm.size != self.H * self.W:
+            raise InvalidParams(f"label map must hold {self.H * self.W} labels, got {lm.size}")
         N.check(self.L.lfdg_set_grid(self.h, view, cell_size, N.ptr(lm)))
 
     # -- sweep / planes / depth
@@ -258,6 +310,8 @@ class DeviceContext:
 
     def set_planes(self, view: int, planes: np.ndarray):
         planes = np.ascontiguousarray(planes, np.float64)
+        gw, gh, _ = self.grid_shape(view)
+        check_shape(planes, (gw * gh, 4), "planes")
         N.check(self.L.lfdg_set_planes(self.h, view, N.ptr(planes)))
 
     def get_planes(self, view: int) -> np.ndarray:
@@ -279,6 +333,8 @@ class DeviceContext:
 
     def set_depth(self, view: int, depth: np.ndarray):
         depth = np.ascontiguousarray(depth, np.float32)
+        if depth.size != self.H * self.W:
+            raise InvalidParams(f"depth map must be [{self.H}][{self.W}], got shape {tuple(depth.shape)}")
         N.check(self.L.lfdg_set_depth(self.h, view, N.ptr(depth)))
 
     # -- refinement

@@ -9,6 +9,14 @@
 // for the FMA variants, read off `objdump -d` of libm.so.6; tables are the
 // libm bytes (libm_tables.h).  tests/test_libm_port.py checks them against the host libm
 // (expf exhaustively over every float, exp on 2e8 samples); tests/test_gpu_math.py on device.
+// Attribution and licence: the algorithms, constants and tables below are derived from the GNU C
+// Library 2.39 (sysdeps/ieee754/dbl-64/e_exp.c + e_exp_data.c, sysdeps/ieee754/flt-32/e_expf.c,
+// e_exp2f_data.c, e_powf.c + e_powf_log2_data.c, s_cbrtf.c), Copyright (C) 1991-2024 Free
+// Software Foundation, Inc., distributed under the GNU Lesser General Public License v2.1 or
+// later (https://www.gnu.org/licenses/lgpl-2.1.html).  The exp / expf / powf routines in glibc
+// originate from ARM Optimized Routines (Copyright (c) 2017-2018 Arm Ltd., MIT licence).  This
+// file is a derivative work under those terms; it is compiled into liblfdg.so only so that the
+// GPU reproduces the host libm bit for bit.
 #pragma once
 
 #include <math.h>

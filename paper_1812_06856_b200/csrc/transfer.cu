@@ -32,6 +32,18 @@ __global__ void k_rgb8_to_lab(const unsigned char* __restrict__ src, float4* __r
 }
 }  // namespace
 
+// The float staging buffer (stage_s.buf) is shared by the serial uploads (upload_images /
+// upload_rgb, compute stream) and the pipelined prefetch (copy stream).  A serial upload while a
+// prefetch is uncommitted would be overwritten by (or overwrite) the staged views, so it is
+// refused; after a serial repack the buffer is marked consumed on the compute stream, so the
+// next prefetch's copy waits for the repack instead of racing it.
+static void staging_acquire(Ctx& c) {
+    if (c.pipe.has_staged) throw Error(LFDG_STATE, "a prefetched upload is still uncommitted");
+}
+static void staging_release(Ctx& c) {
+    if (c.pipe.stream) LFDG_CUDA_CHECK(cudaEventRecord(c.pipe.consumed, c.stream));
+}
+
 // 8-bit sRGB images in ([n][H][W][3] bytes, R G B order), converted like read_image +
 // rgb_to_scaled_lab on the device.
 void upload_rgb8(Ctx& c, int v0, int n, const unsigned char* host) {
@@ -54,6 +66,8 @@ void upload_rgb(Ctx& c, int v0, int n, const float* host) {
     c.require_views();
     if (v0 < 0 || n < 0 || v0 + n > c.V) throw Error(LFDG_STATE, "view range out of bounds");
     if (n == 0) return;
+    if (!host) throw Error(LFDG_STATE, "null images");
+    staging_acquire(c);
     const size_t hw = c.hw();
     StagingScratch& s = c.stage_s;
     s.buf.alloc((size_t)c.V * hw * 3);
@@ -61,12 +75,15 @@ void upload_rgb(Ctx& c, int v0, int n, const float* host) {
     const size_t m = (size_t)n * hw;
     k_rgb_to_lab<<<(unsigned)((m + 255) / 256), 256, 0, c.stream>>>(s.buf.p, c.lab.p + (size_t)v0 * hw, m);
     LFDG_LAUNCHED(&c);
+    staging_release(c);
 }
 
 void upload_images(Ctx& c, int v0, int n, const float* host) {
     c.require_views();
     if (v0 < 0 || n < 0 || v0 + n > c.V) throw Error(LFDG_STATE, "view range out of bounds");
     if (n == 0) return;
+    if (!host) throw Error(LFDG_STATE, "null images");
+    staging_acquire(c);
     const size_t hw = c.hw();
     StagingScratch& s = c.stage_s;
     s.buf.alloc((size_t)c.V * hw * 3);
@@ -74,6 +91,7 @@ void upload_images(Ctx& c, int v0, int n, const float* host) {
     const size_t m = (size_t)n * hw;
     k_repack<<<(unsigned)((m + 255) / 256), 256, 0, c.stream>>>(s.buf.p, c.lab.p + (size_t)v0 * hw, m);
     LFDG_LAUNCHED(&c);
+    staging_release(c);
 }
 
 // ---- pipelined transfers ---------------------------------------------------------------------
@@ -234,18 +252,25 @@ int lfdg_upload_rgb8(lfdg_ctx* p, int v0, int n, const unsigned char* rgb8) {
 
 int lfdg_rgb_to_scaled_lab_gpu(int device, const float* rgb, float* lab, size_t n) {
     try {
+        if (!rgb || !lab) throw lfdg::Error(LFDG_STATE, "null buffer");
         LFDG_CUDA_CHECK(cudaSetDevice(device));
-        float* din = nullptr;
-        float4* dout = nullptr;
-        LFDG_CUDA_CHECK(cudaMalloc(&din, n * 3 * sizeof(float)));
-        LFDG_CUDA_CHECK(cudaMalloc(&dout, n * sizeof(float4)));
-        LFDG_CUDA_CHECK(cudaMemcpy(din, rgb, n * 3 * sizeof(float), cudaMemcpyHostToDevice));
-        lfdg::k_rgb_to_lab<<<(unsigned)((n + 255) / 256), 256>>>(din, dout, n);
+        if (n == 0) return LFDG_OK;
+        cudaStream_t st = nullptr;
+        LFDG_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        struct StreamGuard {
+            cudaStream_t s;
+            ~StreamGuard() { cudaStreamDestroy(s); }
+        } sg{st};
+        lfdg::DevBuf<float> din;   // RAII: freed on every exit path
+        lfdg::DevBuf<float4> dout;
+        din.alloc(n * 3);
+        dout.alloc(n);
+        LFDG_CUDA_CHECK(cudaMemcpyAsync(din.p, rgb, n * 3 * sizeof(float), cudaMemcpyHostToDevice, st));
+        lfdg::k_rgb_to_lab<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(din.p, dout.p, n);
         LFDG_CUDA_CHECK(cudaGetLastError());
-        LFDG_CUDA_CHECK(cudaMemcpy2D(lab, 3 * sizeof(float), dout, sizeof(float4), 3 * sizeof(float), n,
-                                     cudaMemcpyDeviceToHost));
-        cudaFree(din);
-        cudaFree(dout);
+        LFDG_CUDA_CHECK(cudaMemcpy2DAsync(lab, 3 * sizeof(float), dout.p, sizeof(float4), 3 * sizeof(float), n,
+                                          cudaMemcpyDeviceToHost, st));
+        LFDG_CUDA_CHECK(cudaStreamSynchronize(st));
         return LFDG_OK;
     } catch (const lfdg::Error& e) {
         lfdg::set_last_error(e.what());

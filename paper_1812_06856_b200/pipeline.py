@@ -18,7 +18,7 @@ from typing import List, Optional, Tuple
 import numpy as np
 
 from . import _native as N
-from .api import DeviceContext, EnergyParams, SlicParams, SweepParams
+from .api import DeviceContext, EnergyParams, InvalidParams, SlicParams, SweepParams, check_images
 
 GRID_BUFFERS = (N.BUF_LABELS, N.BUF_CX, N.BUF_CY, N.BUF_COLOR, N.BUF_COUNT, N.BUF_MOFF, N.BUF_MPIX, N.BUF_CRAY)
 
@@ -92,6 +92,21 @@ class HotPath:
             torch.cuda.set_stream(self.stream)
             self.ctx.set_stream(self.stream.cuda_stream)
         self.ctx.set_views(images, cams, d_range)
+        self.H, self.W = images.shape[1], images.shape[2]
+
+    def _check_host_images(self, a: np.ndarray, what: str):
+        check_images(a, what, self.H, self.W)
+        if a.shape[0] != self.V:
+            raise InvalidParams(f"{what}: every one of the {self.V} views is uploaded, got {a.shape[0]}")
+
+    def _check_results(self, planes_host, depth_host):
+        nsp = self.ctx.grid_shape(self.v0)[0] * self.ctx.grid_shape(self.v0)[1] if self.n else 0
+        if planes_host is not None and (planes_host.dtype != np.float64 or planes_host.size != self.n * nsp * 4
+                                        or not planes_host.flags.c_contiguous):
+            raise InvalidParams(f"planes_host must be a contiguous float64 [{self.n}][{nsp}][4] array")
+        if depth_host is not None and (depth_host.dtype != np.float32 or depth_host.size != self.n * self.H * self.W
+                                       or not depth_host.flags.c_contiguous):
+            raise InvalidParams(f"depth_host must be a contiguous float32 [{self.n}][{self.H}][{self.W}] array")
 
     # ---- exchange plumbing
     def _tensor(self, which: int):
@@ -141,12 +156,14 @@ class HotPath:
     def upload(self, images_host: np.ndarray):
         """Enqueue the H2D copy of every view's LAB image (replicated on every rank)."""
         images_host = np.ascontiguousarray(images_host, np.float32)
+        self._check_host_images(images_host, "images")
         N.check(N.lib().lfdg_upload_images(self.ctx.h, 0, self.V, N.ptr(images_host)))
 
     def upload_rgb(self, rgb_host: np.ndarray):
         """Enqueue the H2D copy of every view's sRGB image and its conversion to scaled LAB on the
         device (rgb_to_scaled_lab, image.hpp:97-107; the reference does it on the host)."""
         rgb_host = np.ascontiguousarray(rgb_host, np.float32)
+        self._check_host_images(rgb_host, "rgb images")
         N.check(N.lib().lfdg_upload_rgb(self.ctx.h, 0, self.V, N.ptr(rgb_host)))
 
     # ---- pipelined end-to-end transfers (copy stream next to the compute stream)
@@ -154,6 +171,7 @@ class HotPath:
         """Enqueue the H2D copy of every view's LAB image into the staging buffer on the copy
         stream; it overlaps the compute already enqueued.  Install it with commit()."""
         images_host = np.ascontiguousarray(images_host, np.float32)
+        self._check_host_images(images_host, "images")
         N.check(N.lib().lfdg_prefetch_images(self.ctx.h, 0, self.V, N.ptr(images_host)))
 
     def commit(self):
@@ -162,6 +180,7 @@ class HotPath:
     def download_async(self, planes_host: Optional[np.ndarray], depth_host: Optional[np.ndarray]):
         """D2H of this rank's planes / depth on the copy stream, overlapping the next step's SLIC
         (run() makes the next sweep wait for it)."""
+        self._check_results(planes_host, depth_host)
         N.check(N.lib().lfdg_download_results_async(self.ctx.h, self.v0, self.n,
                                                     None if planes_host is None else N.ptr(planes_host),
                                                     None if depth_host is None else N.ptr(depth_host)))
@@ -173,10 +192,12 @@ class HotPath:
         """Enqueue the H2D copy of every view's 8-bit sRGB image (a decoded image file, 1 B per
         channel) and its conversion to scaled LAB on the device (read_image + rgb_to_scaled_lab)."""
         rgb8_host = np.ascontiguousarray(rgb8_host, np.uint8)
+        self._check_host_images(rgb8_host, "rgb8 images")
         N.check(N.lib().lfdg_upload_rgb8(self.ctx.h, 0, self.V, N.ptr(rgb8_host)))
 
     def download(self, planes_host: Optional[np.ndarray], depth_host: Optional[np.ndarray], sync: bool = True):
         """Enqueue the D2H copy of this rank's views' planes [n][nsp][4] and depth [n][H][W]."""
+        self._check_results(planes_host, depth_host)
         N.check(N.lib().lfdg_download_results(self.ctx.h, self.v0, self.n,
                                               None if planes_host is None else N.ptr(planes_host),
                                               None if depth_host is None else N.ptr(depth_host), int(sync)))

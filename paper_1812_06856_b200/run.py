@@ -64,7 +64,7 @@ class PipelineConfig:  # pipeline.hpp:30-66 (the manifest is replaced by in-memo
     dump_every: int = 0
     stages: List[str] = field(default_factory=lambda: list(STAGE_ORDER))
 
-    def validate(self) -> None:  # pipeline.hpp:43-56 (parameter structs are validated by the library)
+    def validate(self) -> None:  # pipeline.hpp:43-56, before any file I/O
         if not self.out_dir:
             raise InvalidParams("output directory required")
         if self.fusion_epsilon < 0 or self.dump_every < 0:
@@ -74,6 +74,9 @@ class PipelineConfig:  # pipeline.hpp:30-66 (the manifest is replaced by in-memo
         for s in self.stages:
             if s not in STAGE_ORDER:
                 raise InvalidParams("unknown stage: " + s)
+        self.slic.validate()
+        self.sweep.validate()
+        self.energy.validate()
 
     def has_stage(self, name: str) -> bool:
         return name in self.stages

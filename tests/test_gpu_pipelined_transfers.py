@@ -63,3 +63,81 @@ def test_commit_without_prefetch_is_a_state_error():
     N.check(N.lib().lfdg_commit_images(dc.h))
     dc.synchronize()
     dc.close()
+
+
+def test_serial_and_pipelined_uploads_mixed():
+    """upload_images (serial, compute stream) and prefetch (copy stream) share the
+    staging buffer.  prefetch(A) -> commit -> run -> upload(B) -> prefetch(C) -> commit must run
+    B's step on B's images and C's step on C's; a serial upload while a prefetch is uncommitted is
+    refused."""
+    import torch
+
+    from paper_1812_06856_b200 import _native as N, api, scenes
+    from paper_1812_06856_b200.pipeline import HotPath, HotPathConfig, estimate_depth
+
+    a = scenes.render_config("C1")
+    sets = [a["lab"], scenes.render_scene("occluder", 3, 320, 240, 320.0, 0.1)["lab"],
+            scenes.render_scene("staircase", 3, 320, 240, 320.0, 0.1)["lab"]]
+    cfg = HotPathConfig(slic=api.SlicParams(12, 0.1, 10), sweep=api.SweepParams(32, 0.05, 0),
+                        energy=api.EnergyParams(iterations=2), seed=0)
+    want = [estimate_depth(x, a["cams"], a["range"], cfg) for x in sets]
+    hp = HotPath(0, a["lab"], a["cams"], a["range"], cfg, use_torch_stream=False)
+    pins = []
+    for x in sets:
+        p = torch.empty(x.size, dtype=torch.float32, pin_memory=True).numpy().reshape(x.shape)
+        p[...] = x
+        pins.append(p)
+    nsp = 27 * 20
+    got = []
+
+    def step():
+        hp.run()
+        pl = np.zeros((3, nsp, 4), np.float64)
+        dp = np.zeros((3, 240, 320), np.float32)
+        hp.download(pl, dp, sync=True)
+        got.append((pl, dp))
+
+    hp.prefetch(pins[0])
+    hp.commit()
+    step()
+    hp.upload(pins[1])   # serial repack from the staging buffer ...
+    hp.prefetch(pins[2])  # ... immediately followed by a prefetch into the same buffer
+    with pytest.raises(api.StateError):
+        hp.upload(pins[1])  # refused while C is staged
+    # B's images are installed; C waits in the staging buffer until commit
+    step()
+    hp.commit()
+    step()
+    hp.close()
+    for k, (pl, dp) in enumerate(got):
+        wp, wd = want[k]
+        assert np.array_equal(pl.view(np.uint64), np.stack(wp).view(np.uint64)), f"set {k} planes"
+        assert np.array_equal(dp.view(np.uint32), wd.view(np.uint32)), f"set {k} depth"
+
+
+def test_wrong_shapes_raise_before_the_abi():
+    from paper_1812_06856_b200 import api, scenes
+    from paper_1812_06856_b200.pipeline import HotPath, HotPathConfig
+
+    a = scenes.render_config("C1")
+    dc = api.DeviceContext(0)
+    with pytest.raises(api.InvalidParams):
+        dc.set_views(a["lab"], a["cams"][:2], a["range"])  # fewer cameras than views
+    with pytest.raises(api.InvalidParams):
+        dc.set_views(a["lab"][..., 0], a["cams"], a["range"])  # [V][H][W]
+    dc.set_views(a["lab"], a["cams"], a["range"])
+    with pytest.raises(api.InvalidParams):
+        dc.update_images(0, np.zeros((1, 240, 320, 4), np.float32))
+    with pytest.raises(api.InvalidParams):
+        dc.update_images(0, np.zeros((1, 120, 320, 3), np.float32))
+    with pytest.raises(api.InvalidParams):
+        dc.upload_rgb(np.zeros((4, 240, 320, 3), np.float32))  # more views than the context holds
+    with pytest.raises(api.InvalidParams):
+        dc.upload_rgb8(np.zeros((1, 240, 321, 3), np.uint8))
+    dc.close()
+    hp = HotPath(0, a["lab"], a["cams"], a["range"], HotPathConfig(), use_torch_stream=False)
+    with pytest.raises(api.InvalidParams):
+        hp.prefetch(a["lab"][:2])
+    with pytest.raises(api.InvalidParams):
+        hp.upload(np.zeros((3, 240, 320, 4), np.float32))
+    hp.close()
