@@ -37,11 +37,38 @@ class Mat {
         return reinterpret_cast<T*>(buf_.data())[static_cast<std::size_t>(y) * cols + x];
     }
 
+    std::vector<unsigned char>& raw() { return buf_; }
+    const std::vector<unsigned char>& raw() const { return buf_; }
+
   private:
     int type_ = 0;
     std::vector<unsigned char> buf_;
 };
 
+#ifndef LFD_STUB_RAW_IO
 inline Mat imread(const std::string&, int) { return Mat(); }
 inline bool imwrite(const std::string&, const Mat&) { return false; }
+#else
+// Raw round-trip stand-in for PNG files (oracle/gpu_acceptance.cpp only): imwrite dumps the Mat
+// (rows, cols, type, pixels) and imread reads it back, so the reference's run_pipeline can
+// write and re-read its own artefacts (acceptance criterion 8).  Not a PNG codec.
+}  // namespace cv
+#include <fstream>
+namespace cv {
+inline Mat imread(const std::string& path, int) {
+    std::ifstream f(path, std::ios::binary);
+    int hdr[3];
+    if (!f.read(reinterpret_cast<char*>(hdr), sizeof(hdr))) return Mat();
+    Mat m(hdr[0], hdr[1], hdr[2]);
+    f.read(reinterpret_cast<char*>(m.raw().data()), static_cast<std::streamsize>(m.raw().size()));
+    return f ? m : Mat();
+}
+inline bool imwrite(const std::string& path, const Mat& m) {
+    std::ofstream f(path, std::ios::binary);
+    const int hdr[3] = {m.rows, m.cols, m.type()};
+    f.write(reinterpret_cast<const char*>(hdr), sizeof(hdr));
+    f.write(reinterpret_cast<const char*>(m.raw().data()), static_cast<std::streamsize>(m.raw().size()));
+    return static_cast<bool>(f);
+}
+#endif
 }  // namespace cv

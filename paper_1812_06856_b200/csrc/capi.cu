@@ -366,7 +366,9 @@ int lfdg_refine_iteration(lfdg_ctx* p, int l, uint64_t* accepted, uint64_t* viol
         if (!c->refine.ready) throw lfdg::Error(LFDG_STATE, "no refine context: call lfdg_make_refine_context");
         if (l < 1) throw lfdg::Error(LFDG_INVALID_PARAMS, "iteration index must be >= 1");
         LFDG_CUDA_CHECK(cudaMemsetAsync(c->counters.p, 0, 2 * sizeof(unsigned long long), c->stream));  // work counters [2..3] accumulate
-        lfdg::refine_iteration(*c, l);
+        // RefineStats requested (violations != null): the reference's independent re-check of
+        // every acceptance (refine.hpp:281-286) runs too
+        lfdg::refine_iteration(*c, l, violations != nullptr);
         if (accepted || violations) {
             unsigned long long h[2];
             LFDG_CUDA_CHECK(cudaMemcpyAsync(h, c->counters.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
@@ -385,7 +387,7 @@ int lfdg_run_refinement(lfdg_ctx* p, uint64_t* accepted, uint64_t* violations) {
         if (!c->refine.ready) throw lfdg::Error(LFDG_STATE, "no refine context: call lfdg_make_refine_context");
         LFDG_CUDA_CHECK(cudaMemsetAsync(c->counters.p, 0, 2 * sizeof(unsigned long long), c->stream));  // work counters [2..3] accumulate
         for (int l = 1; l <= c->refine.params.iterations; ++l) {
-            lfdg::refine_iteration(*c, l);
+            lfdg::refine_iteration(*c, l, violations != nullptr);
             lfdg::rasterize_views(*c, 0, c->V);
         }
         unsigned long long h[2];

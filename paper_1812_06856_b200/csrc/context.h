@@ -114,6 +114,7 @@ struct RefineScratch {
     DevBuf<int> task_counter;  // persistent-warp work counter
     DevBuf<double4> cand;      // per-warp candidate planes
     DevBuf<double> es;         // per-warp smoothness bounds
+    DevBuf<int2> acc;          // per-warp accepted (previous, new) pairs, stats mode
 };
 struct FuseScratch {
     DevBuf<double> xf;  // [V][12] source -> reference transforms
@@ -207,7 +208,7 @@ void sweep_views(Ctx& c, int v0, int n, const lfdg_sweep_params& p, uint64_t see
 void rasterize_views(Ctx& c, int v0, int n);                                   // sweep.cu
 std::vector<int> matching_views(const Ctx& c, int view, int max_neighbors);    // sweep.cu
 void make_refine_tables(Ctx& c, const lfdg_energy_params& p, int sweep_levels);  // refine.cu
-void refine_iteration(Ctx& c, int l);                                            // refine.cu
+void refine_iteration(Ctx& c, int l, bool recheck);                                         // refine.cu
 void upload_images(Ctx& c, int v0, int n, const float* host);                     // transfer.cu
 void upload_rgb8(Ctx& c, int v0, int n, const unsigned char* host);              // transfer.cu
 void prefetch_images(Ctx& c, int v0, int n, const float* host);                  // transfer.cu

@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <type_traits>
 
 #include "context.h"
 #include "glibc_math.cuh"
@@ -171,6 +172,7 @@ struct PixGeo {
 struct WarpSmem {
     double4* cand;  // [cap]   (global scratch)
     double* es;     // [cap]   (global scratch)
+    int2* acc;      // [cap]   (global scratch) accepted (previous, new) candidate pairs of the task (recheck)
     void* tg;       // [N] TargetRow, or TargetFlat for kFlat
     PixGeo* geo;    // [32] geometry of the current pixel chunk (one entry per lane)
     double2* pc;    // [cw][ways + 1] lane-private photo-weight cache rows: (weight, raster word); the
@@ -432,10 +434,11 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
 // accepted either) — so the accepted planes and the count are the reference's.
 // init: cand[0] is the current plane and its energy initialises e_cur (refine.hpp:277).
 // current: index in cand of the running plane.
-template <bool kIdR, bool kCanonK, int kFlat>
+template <bool kIdR, bool kCanonK, int kFlat, bool kRecheck>
 __device__ __forceinline__ void greedy(const RefineArgs& a, const WarpSmem& w, int base, int n, int v, int sp, int m0,
                                        int n_members, bool init, double& e_cur, int& current, unsigned& accepted,
                                        unsigned long long& pix_evals, unsigned& cand_evals) {
+    // (accepted also indexes w.acc: the recheck list of this task's acceptances)
     const int lane = threadIdx.x & 31;
     const bool prune = a.use_s && a.use_c;
     const int G = lanes_per_candidate(a.N, kFlat);
@@ -486,6 +489,7 @@ __device__ __forceinline__ void greedy(const RefineArgs& a, const WarpSmem& w, i
             if (init) {
                 e_cur = e;
             } else if ((k == 0 || passes(c)) && e > e_cur) {
+                if (kRecheck && lane == 0) w.acc[accepted] = make_int2(current, c);
                 e_cur = e;
                 current = c;
                 accepted++;
@@ -534,15 +538,63 @@ __device__ void smoothness_all(const RefineArgs& a, const WarpSmem& w, int base,
     __syncwarp();
 }
 
+// RefineStats' independent re-check (refine.hpp:281-286): for every acceptance of the task,
+// energy(candidate) and energy(previous plane) are evaluated again from scratch against the
+// snapshot — smoothness_term and consistency_term recomputed, multiplied in energy()'s order
+// (refine.hpp:201-207) — and an acceptance whose candidate does not strictly beat its
+// predecessor counts as a violation.  Only in stats mode (the reference pays the same price).
+template <bool kIdR, bool kCanonK, int kFlat>
+__device__ __forceinline__ unsigned recheck_acceptances(const RefineArgs& a, const WarpSmem& w, int v, int sp, int m0, int n_members,
+                                        unsigned n_acc) {
+    const int lane = threadIdx.x & 31;
+    const int G = lanes_per_candidate(a.N, kFlat);
+    const int slots = 32 / G;
+    unsigned violations = 0;
+    for (unsigned k = 0; k < n_acc; ++k) {
+        const int2 pr = w.acc[k];  // (previous, candidate)
+        double e[2];
+        for (int j = 0; j < 2; ++j) {
+            const int idx = j == 0 ? pr.x : pr.y;
+            double es = 1.0;
+            if (a.use_s) {
+                const double4 p = w.cand[idx];
+                es = smoothness_group(a, v, sp, p, true);  // every 8-lane group computes the same value
+            }
+            e[j] = es;
+        }
+        double ec[2] = {1.0, 1.0};
+        if (a.use_c) {
+            if (slots >= 2) {
+                const int mine = lane / G == 0 ? pr.x : pr.y;
+                const double r = consistency_pair<kIdR, kCanonK, kFlat>(a, w, v, sp, w.cand[mine], m0, n_members);
+                ec[0] = __shfl_sync(LFDG_FULL_MASK, r, 0);
+                ec[1] = __shfl_sync(LFDG_FULL_MASK, r, G);
+            } else {
+                ec[0] = consistency_pair<kIdR, kCanonK, kFlat>(a, w, v, sp, w.cand[pr.x], m0, n_members);
+                ec[1] = consistency_pair<kIdR, kCanonK, kFlat>(a, w, v, sp, w.cand[pr.y], m0, n_members);
+            }
+        }
+        double en[2];
+        for (int j = 0; j < 2; ++j) {  // energy(): e = 1; e *= E_s; e *= E_c
+            double x = 1.0;
+            if (a.use_s) x *= e[j];
+            if (a.use_c) x *= ec[j];
+            en[j] = x;
+        }
+        if (!(en[1] > en[0])) ++violations;
+    }
+    return violations;
+}
+
 // Persistent kernel: each warp pulls (view, superpixel) tasks from a global counter and runs
 // refine_iteration's task body (refine.hpp:269-320) for it.
 // Resident CTAs per SM (register budget): 8 (64 registers), or 7 in the many-target mode,
 // whose latency-bound gathers gain more from the registers and the L1 than from an 8th CTA
 // (C4: 111 -> 100 ms/view; C3 prefers 8: 104.7 vs 106.8 ms per refine launch).
 __host__ __device__ constexpr int refine_min_blocks(int flat_mode) { return flat_mode == 3 ? 7 : 8; }
-template <bool kIdR, bool kCanonK, int kFlat>
+template <bool kIdR, bool kCanonK, int kFlat, bool kRecheck>
 __global__ void __launch_bounds__(128, refine_min_blocks(kFlat))
-    k_refine(RefineArgs a, int n_tasks, int* task_counter, int cap, double4* g_cand, double* g_es) {
+    k_refine(RefineArgs a, int n_tasks, int* task_counter, int cap, double4* g_cand, double* g_es, int2* g_acc) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -556,10 +608,11 @@ __global__ void __launch_bounds__(128, refine_min_blocks(kFlat))
     w.res = reinterpret_cast<double*>(w.geo + 32);
     w.cand = g_cand + (size_t)gwarp * cap;
     w.es = g_es + (size_t)gwarp * cap;
+    w.acc = g_acc + (size_t)gwarp * cap;
 
     unsigned long long pix_evals = 0;
     unsigned cand_evals = 0;
-    unsigned long long accepted_total = 0;
+    unsigned long long accepted_total = 0, violations_total = 0;
     while (true) {
         int task = 0;
         if (lane == 0) task = atomicAdd(task_counter, 1);
@@ -614,7 +667,7 @@ __global__ void __launch_bounds__(128, refine_min_blocks(kFlat))
         __syncwarp();
         if (a.use_s) smoothness_all(a, w, 0, 1, v, sp);
         mark_repeats(a, w, 0, 1);
-        greedy<kIdR, kCanonK, kFlat>(a, w, 0, 1, v, sp, m0, n_members, true, e_cur, current, accepted, pix_evals,
+        greedy<kIdR, kCanonK, kFlat, kRecheck>(a, w, 0, 1, v, sp, m0, n_members, true, e_cur, current, accepted, pix_evals,
                                      cand_evals);
 
         // ---- phase A: grid_neighbors(Kernel) order (superpixel.hpp:318-343), re-anchored
@@ -661,7 +714,7 @@ __global__ void __launch_bounds__(128, refine_min_blocks(kFlat))
         __syncwarp();
         if (a.use_s) smoothness_all(a, w, 1, n_cand, v, sp);
         mark_repeats(a, w, 1, 1 + n_cand);
-        greedy<kIdR, kCanonK, kFlat>(a, w, 1, n_cand, v, sp, m0, n_members, false, e_cur, current, accepted, pix_evals,
+        greedy<kIdR, kCanonK, kFlat, kRecheck>(a, w, 1, n_cand, v, sp, m0, n_members, false, e_cur, current, accepted, pix_evals,
                                      cand_evals);
 
         // ---- phase B: normal_candidates (refine.hpp:213-242) at the phase-A depth
@@ -707,15 +760,20 @@ __global__ void __launch_bounds__(128, refine_min_blocks(kFlat))
             const int nn = __popc(m);
             if (a.use_s) smoothness_all(a, w, 1 + n_cand, nn, v, sp);
             mark_repeats(a, w, 1 + n_cand, 1 + n_cand + nn);
-            greedy<kIdR, kCanonK, kFlat>(a, w, 1 + n_cand, nn, v, sp, m0, n_members, false, e_cur, current, accepted,
+            greedy<kIdR, kCanonK, kFlat, kRecheck>(a, w, 1 + n_cand, nn, v, sp, m0, n_members, false, e_cur, current, accepted,
                                          pix_evals, cand_evals);
         }
         if (lane == 0) a.out[vs + sp] = w.cand[current];
         accepted_total += accepted;
+        if (kRecheck && accepted) {
+            __syncwarp();
+            violations_total += recheck_acceptances<kIdR, kCanonK, kFlat>(a, w, v, sp, m0, n_members, accepted);
+        }
         __syncwarp();
     }
     if (lane == 0) {
         if (accepted_total) atomicAdd(&a.counters[0], accepted_total);
+        if (violations_total) atomicAdd(&a.counters[1], violations_total);
         atomicAdd(&a.counters[2], pix_evals);
         atomicAdd(&a.counters[3], (unsigned long long)cand_evals);
     }
@@ -848,7 +906,7 @@ void make_refine_tables(Ctx& c, const lfdg_energy_params& p, int sweep_levels) {
     t.ready = true;
 }
 
-void refine_iteration(Ctx& c, int l) {
+void refine_iteration(Ctx& c, int l, bool recheck) {
     RefineTables& t = c.refine;
     const lfdg_energy_params& p = t.params;
     for (int v = 0; v < c.V; ++v)
@@ -940,31 +998,43 @@ void refine_iteration(Ctx& c, int l) {
             rd.task_counter.alloc(1);
             rd.cand.alloc((size_t)blocks * 4 * cap);
             rd.es.alloc((size_t)blocks * 4 * cap);
+            rd.acc.alloc((size_t)blocks * 4 * cap);
             LFDG_CUDA_CHECK(cudaMemsetAsync(rd.task_counter.p, 0, sizeof(int), c.stream));
-            kernel<<<blocks, 128, smem, c.stream>>>(a, n_tasks, rd.task_counter.p, cap, rd.cand.p, rd.es.p);
+            kernel<<<blocks, 128, smem, c.stream>>>(a, n_tasks, rd.task_counter.p, cap, rd.cand.p, rd.es.p, rd.acc.p);
         };
         // kFlat (flat above): every rotation I, canonical and identical K, every camera centre at
         // z = 0 (then every rel_trans.z = 0): the rectified / grid rigs of the fixtures.
+        // kRecheck (stats mode): a separate instantiation carries the re-check, so the hot
+        // variant's register allocation is untouched by it
+        auto pick = [&](auto rc) {
+            constexpr bool R = decltype(rc)::value;
+            if (flat) {
+                if (a.row_inv)
+                    launch(k_refine<true, true, 2, R>);
+                else if (ras8)
+                    launch(k_refine<true, true, 3, R>);
+                else
+                    launch(k_refine<true, true, 1, R>);
+            } else if (c.identity_rot && c.canonical_k) {
+                launch(k_refine<true, true, 0, R>);
+            } else if (c.identity_rot) {
+                launch(k_refine<true, false, 0, R>);
+            } else if (c.canonical_k) {
+                launch(k_refine<false, true, 0, R>);
+            } else {
+                launch(k_refine<false, false, 0, R>);
+            }
+        };
         if (flat) {
             a.uK00 = c.cams[0].K[0];
             a.uK02 = c.cams[0].K[2];
             a.uK11 = c.cams[0].K[4];
             a.uK12 = c.cams[0].K[5];
-            if (a.row_inv)
-                launch(k_refine<true, true, 2>);
-            else if (ras8)
-                launch(k_refine<true, true, 3>);
-            else
-                launch(k_refine<true, true, 1>);
-        } else if (c.identity_rot && c.canonical_k) {
-            launch(k_refine<true, true, 0>);
-        } else if (c.identity_rot) {
-            launch(k_refine<true, false, 0>);
-        } else if (c.canonical_k) {
-            launch(k_refine<false, true, 0>);
-        } else {
-            launch(k_refine<false, false, 0>);
         }
+        if (recheck)
+            pick(std::true_type{});
+        else
+            pick(std::false_type{});
         LFDG_LAUNCHED(&c);
         LFDG_CUDA_CHECK(cudaMemcpyAsync(c.planes.p + (size_t)rv0 * c.nsp, c.planes_next.p + (size_t)rv0 * c.nsp,
                                         (size_t)rn * c.nsp * sizeof(double4), cudaMemcpyDeviceToDevice, c.stream));
