@@ -188,6 +188,9 @@ int lfdg_run_refinement(lfdg_ctx* ctx, uint64_t* accepted, uint64_t* violations)
 /* Work counters accumulated by refine_iteration since the last reset: evaluated
  * (candidate, target, member pixel) triples of pair_stats and evaluated candidates. */
 int lfdg_refine_work(lfdg_ctx* ctx, uint64_t* pixel_evals, uint64_t* candidate_evals, int reset);
+/* Diagnostic: (candidate, target, member pixel) triples executed by idle candidate slots of the
+ * refinement kernel (slots of a speculative group with no surviving candidate to evaluate). */
+int lfdg_refine_idle_work(lfdg_ctx* ctx, uint64_t* idle_pixel_evals, int reset);
 /* min_neighbor_similarity table of make_refine_context (refine.hpp:71), [nsp] floats. */
 int lfdg_get_min_nb_sim(lfdg_ctx* ctx, int view, float* out);
 

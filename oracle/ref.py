@@ -81,6 +81,7 @@ def lib():
     L.ref_sweep_sample.argtypes = [P, I, P, I, I, F, I, U64, I, P]
     L.ref_refine_tasks.argtypes = [P, I, P, P, I, I, P, P, P, P]
     L.ref_fuse_all.argtypes = [P, D, I, P]
+    L.ref_task_candidates.argtypes = [P, I, I, I, I, P, P, P, P, P]
     L.ref_gather_candidates.argtypes = [P, I, P, P, P, C.c_int64, P]
     L.ref_bad_pixel_rate.restype = D
     L.ref_bad_pixel_rate.argtypes = [I, I, I, P, P, I, P, D, D, D, I, D]
@@ -164,6 +165,18 @@ class Session:
         if counts:
             return out, int(acc[0]), int(acc[1]), int(acc[2])
         return out, int(acc[0])
+
+    def task_candidates(self, l, view, sp, max_out=512):
+        """Analysis helper: (e_init, planes [k][4], E_s [k], E_c [k], phase [k]) of one task."""
+        planes = np.zeros((max_out, 4), np.float64)
+        es = np.zeros(max_out, np.float64)
+        ec = np.zeros(max_out, np.float64)
+        ph = np.zeros(max_out, np.int32)
+        e0 = np.zeros(1, np.float64)
+        k = self.L.ref_task_candidates(self.h, l, view, sp, max_out, _p(planes), _p(es), _p(ec), _p(ph), _p(e0))
+        if k < 0:
+            _check(1)
+        return float(e0[0]), planes[:k], es[:k], ec[:k], ph[:k]
 
     def fuse_all(self, epsilon, workers=1):
         out = np.zeros((self.V, self.H, self.W), np.float32)

@@ -527,4 +527,62 @@ int ref_refine_tasks(void* p, int l, const int* views, const int* sps, int n, in
     });
 }
 
+// Analysis helper (not a parity path): every candidate of one refine_iteration task in the
+// reference's order (refine.hpp:305-318) with its smoothness and consistency terms computed
+// unconditionally from the snapshot; phase 1 = propagation, 2 = normals (at the phase-A winner's
+// depth, found by the reference's greedy).  planes_out [max][4], es/ec [max]; returns the count.
+int ref_task_candidates(void* p, int l, int v, int sp, int max_out, double* planes_out, double* es_out,
+                        double* ec_out, int* phase_out, double* e_init) {
+    auto* s = static_cast<Session*>(p);
+    int count = 0;
+    const int rc = guarded([&] {
+        const RefineContext& ctx = *s->ctx;
+        const MultiViewSet& mvs = *ctx.mvs;
+        const PlaneMap& state = s->state;
+        const int kernel_px = static_cast<int>(ctx.params.size_init / static_cast<double>(l));
+        const int kernel_step =
+            std::max(1, static_cast<int>(std::lround(ctx.params.steps_init / static_cast<double>(l))));
+        const SuperpixelGrid& grid = ctx.grid(v);
+        const PinholeCamera& cam = mvs.cameras[v];
+        const Vec2 centroid(grid.sp[sp].cx, grid.sp[sp].cy);
+        SuperpixelPlane current = state.planes[v][sp];
+        double e_cur = energy(ctx, v, sp, current, state);
+        *e_init = e_cur;
+        auto record = [&](const SuperpixelPlane& c, int phase) {
+            if (count >= max_out) return;
+            plane_to(c, planes_out + 4 * count);
+            es_out[count] = smoothness_term(ctx, v, sp, c, state);
+            ec_out[count] = consistency_term(ctx, v, sp, c, state);
+            phase_out[count] = phase;
+            ++count;
+        };
+        auto greedy = [&](const SuperpixelPlane& c) {
+            if (c.depth == current.depth && c.normal == current.normal) return;
+            if (c.depth < mvs.range.d_min || c.depth > mvs.range.d_max) return;
+            const double e = energy(ctx, v, sp, c, state);
+            if (e > e_cur) {
+                current = c;
+                e_cur = e;
+            }
+        };
+        for (const std::int32_t nb : grid_neighbors(grid, sp, NeighborPattern::Kernel, kernel_px, kernel_step)) {
+            const SuperpixelPlane& nb_plane = state.planes[v][nb];
+            const Vec2 nb_centroid(grid.sp[nb].cx, grid.sp[nb].cy);
+            const auto d = plane_depth_at(cam, nb_plane, nb_centroid, centroid);
+            if (!d || *d <= 0) continue;
+            const SuperpixelPlane c{*d, nb_plane.normal};
+            if (c.depth < mvs.range.d_min || c.depth > mvs.range.d_max) continue;
+            record(c, 1);
+            greedy(c);
+        }
+        for (const Vec3& nrm : normal_candidates(ctx, v, sp, state)) {
+            const SuperpixelPlane c{current.depth, nrm};
+            if (c.depth < mvs.range.d_min || c.depth > mvs.range.d_max) continue;
+            record(c, 2);
+            greedy(c);
+        }
+    });
+    return rc == 0 ? count : -1;
+}
+
 }  // extern "C"

@@ -64,7 +64,7 @@ EXPORTED = [
     "lfdg_set_depth", "lfdg_make_refine_context", "lfdg_set_refine_views", "lfdg_refine_iteration",
     "lfdg_run_refinement", "lfdg_get_min_nb_sim", "lfdg_device_buffer", "lfdg_mark_views_ready",
     "lfdg_selftest_exp", "lfdg_selftest_expf", "lfdg_render_scene", "lfdg_rgb_to_scaled_lab",
-    "lfdg_upload_images", "lfdg_download_results", "lfdg_selftest_fp64_peak", "lfdg_refine_work", "lfdg_selftest_exp_nonpos",
+    "lfdg_upload_images", "lfdg_download_results", "lfdg_selftest_fp64_peak", "lfdg_refine_work", "lfdg_refine_idle_work", "lfdg_selftest_exp_nonpos",
     "lfdg_fuse_views", "lfdg_get_fused", "lfdg_gather_candidates", "lfdg_stability_fuse", "lfdg_upload_rgb",
     "lfdg_rgb_to_scaled_lab_gpu", "lfdg_eval_bad_pixel", "lfdg_debug_guard_enabled", "lfdg_debug_check_guards",
     "lfdg_debug_guard_selftest", "lfdg_upload_rgb8", "lfdg_prefetch_images", "lfdg_commit_images",
@@ -151,6 +151,7 @@ def lib():
         "lfdg_download_results": (I, [P, I, I, P, P, I]),
         "lfdg_selftest_fp64_peak": (I, [I, C.POINTER(D)]),
         "lfdg_refine_work": (I, [P, PU64, PU64, I]),
+        "lfdg_refine_idle_work": (I, [P, PU64, I]),
         "lfdg_selftest_exp_nonpos": (I, [I, P, P, C.c_size_t]),
         "lfdg_fuse_views": (I, [P, I, I, D]),
         "lfdg_get_fused": (I, [P, I, P]),

@@ -366,6 +366,12 @@ class DeviceContext:
         N.check(self.L.lfdg_refine_work(self.h, C.byref(a), C.byref(b), int(reset)))
         return a.value, b.value
 
+    def refine_idle_work(self, reset: bool = True) -> int:
+        """Pixel-evaluations executed by idle candidate slots (diagnostic)."""
+        a = C.c_uint64()
+        N.check(self.L.lfdg_refine_idle_work(self.h, C.byref(a), int(reset)))
+        return a.value
+
     # -- fusion (fusion.hpp:31-100)
     def fuse_views(self, epsilon: float, v0: int = 0, n: Optional[int] = None):
         N.check(self.L.lfdg_fuse_views(self.h, v0, self.V - v0 if n is None else n, float(epsilon)))

@@ -66,7 +66,7 @@ int lfdg_create(int device, lfdg_ctx** out) {
         }
         c->stream = c->own_stream;
         cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
-        c->counters.alloc(4);
+        c->counters.alloc(8);
         *out = reinterpret_cast<lfdg_ctx*>(c);
     });
 }
@@ -395,6 +395,18 @@ int lfdg_run_refinement(lfdg_ctx* p, uint64_t* accepted, uint64_t* violations) {
         LFDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
         if (accepted) *accepted = h[0];
         if (violations) *violations = h[1];
+    });
+}
+
+int lfdg_refine_idle_work(lfdg_ctx* p, uint64_t* idle_pixel_evals, int reset) {
+    return guarded([&] {
+        auto* c = C(p);
+        activate(c);
+        unsigned long long h = 0;
+        LFDG_CUDA_CHECK(cudaMemcpyAsync(&h, c->counters.p + 4, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+        LFDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        if (idle_pixel_evals) *idle_pixel_evals = h;
+        if (reset) LFDG_CUDA_CHECK(cudaMemsetAsync(c->counters.p + 4, 0, sizeof(unsigned long long), c->stream));
     });
 }
 

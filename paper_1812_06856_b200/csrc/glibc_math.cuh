@@ -214,6 +214,30 @@ LFDG_HD double exp_nonpos(double x) {
 }
 
 
+#if defined(__CUDACC__)
+// exp_nonpos split for the refinement's hot loop: exp_nonpos_in_core(x) tells, from the high
+// word alone (integer pipe), whether x lies in (-512, -2^-54] where exp_nonpos takes neither
+// early exit nor the specialcase; exp_nonpos_core(x) is exp_nonpos's main path for that
+// range (the same operations and constants, so the same result).  Other x go to exp_nonpos.
+__device__ __forceinline__ bool exp_nonpos_in_core(double x) {
+    return (unsigned)__double2hiint(x) - 0xBC900000u < 0x03F00000u;  // hi in [hi(-2^-54), hi(-512))
+}
+__device__ __forceinline__ double exp_nonpos_core(double x) {
+    double kd = fma_(x, LFDG_EXPC(0), LFDG_EXPC(1));
+    const uint64_t ki = as_u64(kd);
+    kd = kd - LFDG_EXPC(1);
+    const double r = fma_(kd, LFDG_EXPC(3), fma_(kd, LFDG_EXPC(2), x));
+    const unsigned idx = 2u * (unsigned)(ki & 127u);
+    const ulonglong2 te = __ldg(reinterpret_cast<const ulonglong2*>(&kExpTabDev[idx]));  // (tail, sbits)
+    const double tail = as_f64(te.x);
+    const uint64_t sbits = te.y + (ki << 45);
+    const double r2 = r * r;
+    const double tmp = fma_(r2 * r2, fma_(r, LFDG_EXPC(7), LFDG_EXPC(6)), fma_(fma_(r, LFDG_EXPC(5), LFDG_EXPC(4)), r2, r + tail));
+    const double scale = as_f64(sbits);
+    return fma_(scale, tmp, scale);
+}
+#endif
+
 // __expf_fma (glibc sysdeps/ieee754/flt-32/e_expf.c, x86-64 FMA build).
 LFDG_HD float expf(float x) {
     const double kShift = 0x1.8p+52;

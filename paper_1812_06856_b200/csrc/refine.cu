@@ -84,6 +84,14 @@ __device__ __forceinline__ int lround_int(double x) {
 // lround(h / z) the slow way (division, then lround), out of line: fast_lround's rare fallback.
 __device__ __noinline__ int lround_div(double h, double z) { return lround_int(h / z); }
 
+// exp of the visibility term (refine.hpp:158): glibc's main path inline when the argument is in
+// its range (integer test on the high word), the full glibc path (early exits, specialcase) out of
+// line otherwise — the same function as libm::exp_nonpos.
+__device__ __noinline__ double exp_vis_slow(double x) { return libm::exp_nonpos(x); }
+__device__ __forceinline__ double exp_vis(double x) {
+    return libm::exp_nonpos_in_core(x) ? libm::exp_nonpos_core(x) : exp_vis_slow(x);
+}
+
 // depth_consistency (refine.hpp:34-37)
 __device__ __forceinline__ double depth_consistency(double d1, double d2, double two_sigma2) {
     const double r = 1.0 / d1 - 1.0 / d2;
@@ -146,6 +154,18 @@ __device__ __forceinline__ bool fast_lround(double q, int& out) {
     return true;
 }
 
+// fast_lround for the kFlat hot loop: the integer is read off q + 1.5 * 2^52 when that sum lies in
+// [2^52 * 1.5, 2^52 * 1.5 + 2^32) (hi word 0x43380000: 0 <= lround(q) < 2^32), else -1 (outside any
+// image: q < -0.5 or q >= 2^32); within 2^-28 of a half-integer it returns false and the caller
+// divides exactly.  |q| < 2^20 whenever the result can be inside an image (W, H <= 2^20, checked
+// on the host), so the error bound of fast_lround applies.
+__device__ __forceinline__ bool fast_lround_img(double q, int& out) {
+    const double t = q + 0x1.8p52;
+    const double d = q - (t - 0x1.8p52);
+    out = __double2hiint(t) == 0x43380000 ? __double2loint(t) : -1;
+    return fabs(d) < 0.5 - 0x1p-28;
+}
+
 // Per-warp shared-memory slice.  Candidate planes / upper bounds live in a per-warp global
 // scratch row (L1-resident); the per-task target table, the per-pixel geometry of the current
 // pixel chunk, the photo-weight cache and the per-target results are shared memory.
@@ -163,11 +183,13 @@ struct TargetFlat {  // kFlat: R = I, t.z = 0 and the shared K make everything b
 // Target-independent part of pair_stats' transfer for one member pixel (refine.hpp:131-137):
 // s v, and for kFlat (every R = I, every t.z = 0, one shared K) z = s, 1/z, K02 z, K12 z and,
 // for a linear rig, the rounded target row.
-struct PixGeo {
-    double sv0, sv1, sv2;
-    double f_inv, f_kz0, f_kz1;
+struct __align__(16) PixGeo {  // laid out for 16-byte shared loads of the pairs the hot loop reads together
+    double sv0, f_kz0;
+    double f_inv, sv2;
+    double sv1, f_kz1;
     int f_py;
     int ok;
+    int pad[2];
 };
 struct WarpSmem {
     double4* cand;  // [cap]   (global scratch)
@@ -305,12 +327,12 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
                     if (!qq->ok) return false;
                     int px, py;
                     const double hx = a.uK00 * (qq->sv0 + T0) + qq->f_kz0;
-                    if (!fast_lround(hx * qq->f_inv, px)) px = lround_div(hx, qq->sv2);
+                    if (!fast_lround_img(hx * qq->f_inv, px)) px = lround_div(hx, qq->sv2);
                     if (kFlat == 2) {
                         py = qq->f_py;
                     } else {
                         const double hy = a.uK11 * (qq->sv1 + T1) + qq->f_kz1;
-                        if (!fast_lround(hy * qq->f_inv, py)) py = lround_div(hy, qq->sv2);
+                        if (!fast_lround_img(hy * qq->f_inv, py)) py = lround_div(hy, qq->sv2);
                     }
                     if ((unsigned)px >= (unsigned)a.W || (unsigned)py >= (unsigned)a.H) return false;
                     // tgrid.label(px, py) and snapshot.depth[t](px, py) (refine.hpp:146-152) in one
@@ -352,7 +374,7 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
                     if (td <= 0) continue;  // no target depth: not in X or Y
                     if (zt <= (double)td * (1.0 + 1e-6)) {
                         const double rr = inv_z - (kFlat == 3 ? 1.0 / (double)td : __hiloint2double(r.w, r.z));
-                        vis_sum += libm::exp_nonpos(-rr * rr * a.inv_two_sigma2);
+                        vis_sum += exp_vis(-rr * rr * a.inv_two_sigma2);
                         ++x_count;
                     } else {
                         y_nonempty = true;
@@ -403,7 +425,7 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
                     if (td <= 0) continue;  // no target depth: not in X or Y
                     if (zt <= (double)td * (1.0 + 1e-6)) {
                         const double rr = inv_z - __hiloint2double(r.w, r.z);
-                        vis_sum += libm::exp_nonpos(-rr * rr * a.inv_two_sigma2);
+                        vis_sum += exp_vis(-rr * rr * a.inv_two_sigma2);
                         ++x_count;
                     } else {
                         y_nonempty = true;
@@ -437,7 +459,8 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
 template <bool kIdR, bool kCanonK, int kFlat, bool kRecheck>
 __device__ __forceinline__ void greedy(const RefineArgs& a, const WarpSmem& w, int base, int n, int v, int sp, int m0,
                                        int n_members, bool init, double& e_cur, int& current, unsigned& accepted,
-                                       unsigned long long& pix_evals, unsigned& cand_evals) {
+                                       unsigned long long& pix_evals, unsigned& cand_evals,
+                                       unsigned long long& idle_evals) {
     // (accepted also indexes w.acc: the recheck list of this task's acceptances)
     const int lane = threadIdx.x & 31;
     const bool prune = a.use_s && a.use_c;
@@ -455,23 +478,26 @@ __device__ __forceinline__ void greedy(const RefineArgs& a, const WarpSmem& w, i
         return w.es[idx] != -INFINITY && (init || !prune || w.es[idx] * w.m_task > e_cur);
     };
     while (next < n) {
-        const int idx = next + lane;
-        unsigned m = __ballot_sync(LFDG_FULL_MASK, idx < n && passes(idx));
-        if (!m) {
-            next += 32;
-            continue;
+        // the next `slots` surviving candidates in index order (lane group k evaluates the k-th),
+        // gathered over as many 32-candidate windows as it takes
+        int cnt = 0, first = -1, mine = -1;
+        while (cnt < slots && next < n) {
+            const int idx = next + lane;
+            unsigned m = __ballot_sync(LFDG_FULL_MASK, idx < n && passes(idx));
+            int last = -1;
+            while (m && cnt < slots) {
+                const int ck = next + __ffs(m) - 1;
+                m &= m - 1;
+                if (lane / G == cnt) mine = ck;
+                if (cnt == 0) first = ck;
+                last = ck;
+                ++cnt;
+            }
+            next = cnt == slots && last >= 0 ? last + 1 : next + 32;
         }
-        // the next `slots` surviving candidates, in index order; lane group k evaluates the k-th
-        const int first = next + __ffs(m) - 1;
-        int cnt = 0, last = 0, mine = first;  // idle groups repeat the first candidate
-        for (int k = 0; k < slots && m; ++k) {
-            const int ck = next + __ffs(m) - 1;
-            m &= m - 1;
-            if (lane / G == k) mine = ck;
-            last = ck;
-            ++cnt;
-        }
-        next = last + 1;
+        if (cnt == 0) continue;
+        if (mine < 0) mine = first;  // idle groups repeat the first candidate
+        idle_evals += (unsigned long long)(slots - cnt) * a.N * n_members;
         double ec = 0;
         if (a.use_c) {
             ec = consistency_pair<kIdR, kCanonK, kFlat>(a, w, v, sp, w.cand[mine], m0, n_members);
@@ -591,7 +617,10 @@ __device__ __forceinline__ unsigned recheck_acceptances(const RefineArgs& a, con
 // Resident CTAs per SM (register budget): 8 (64 registers), or 7 in the many-target mode,
 // whose latency-bound gathers gain more from the registers and the L1 than from an 8th CTA
 // (C4: 111 -> 100 ms/view; C3 prefers 8: 104.7 vs 106.8 ms per refine launch).
-__host__ __device__ constexpr int refine_min_blocks(int flat_mode) { return flat_mode == 3 ? 7 : 8; }
+#ifndef LFDG_REFINE_MINB
+#define LFDG_REFINE_MINB 8
+#endif
+__host__ __device__ constexpr int refine_min_blocks(int flat_mode) { return flat_mode == 3 ? 7 : LFDG_REFINE_MINB; }
 template <bool kIdR, bool kCanonK, int kFlat, bool kRecheck>
 __global__ void __launch_bounds__(128, refine_min_blocks(kFlat))
     k_refine(RefineArgs a, int n_tasks, int* task_counter, int cap, double4* g_cand, double* g_es, int2* g_acc) {
@@ -612,7 +641,7 @@ __global__ void __launch_bounds__(128, refine_min_blocks(kFlat))
 
     unsigned long long pix_evals = 0;
     unsigned cand_evals = 0;
-    unsigned long long accepted_total = 0, violations_total = 0;
+    unsigned long long accepted_total = 0, violations_total = 0, idle_evals = 0;
     while (true) {
         int task = 0;
         if (lane == 0) task = atomicAdd(task_counter, 1);
@@ -668,7 +697,7 @@ __global__ void __launch_bounds__(128, refine_min_blocks(kFlat))
         if (a.use_s) smoothness_all(a, w, 0, 1, v, sp);
         mark_repeats(a, w, 0, 1);
         greedy<kIdR, kCanonK, kFlat, kRecheck>(a, w, 0, 1, v, sp, m0, n_members, true, e_cur, current, accepted, pix_evals,
-                                     cand_evals);
+                                     cand_evals, idle_evals);
 
         // ---- phase A: grid_neighbors(Kernel) order (superpixel.hpp:318-343), re-anchored
         const int gx = sp % a.gw, gy = sp / a.gw;
@@ -715,7 +744,7 @@ __global__ void __launch_bounds__(128, refine_min_blocks(kFlat))
         if (a.use_s) smoothness_all(a, w, 1, n_cand, v, sp);
         mark_repeats(a, w, 1, 1 + n_cand);
         greedy<kIdR, kCanonK, kFlat, kRecheck>(a, w, 1, n_cand, v, sp, m0, n_members, false, e_cur, current, accepted, pix_evals,
-                                     cand_evals);
+                                     cand_evals, idle_evals);
 
         // ---- phase B: normal_candidates (refine.hpp:213-242) at the phase-A depth
         {
@@ -761,7 +790,7 @@ __global__ void __launch_bounds__(128, refine_min_blocks(kFlat))
             if (a.use_s) smoothness_all(a, w, 1 + n_cand, nn, v, sp);
             mark_repeats(a, w, 1 + n_cand, 1 + n_cand + nn);
             greedy<kIdR, kCanonK, kFlat, kRecheck>(a, w, 1 + n_cand, nn, v, sp, m0, n_members, false, e_cur, current, accepted,
-                                         pix_evals, cand_evals);
+                                         pix_evals, cand_evals, idle_evals);
         }
         if (lane == 0) a.out[vs + sp] = w.cand[current];
         accepted_total += accepted;
@@ -776,6 +805,7 @@ __global__ void __launch_bounds__(128, refine_min_blocks(kFlat))
         if (violations_total) atomicAdd(&a.counters[1], violations_total);
         atomicAdd(&a.counters[2], pix_evals);
         atomicAdd(&a.counters[3], (unsigned long long)cand_evals);
+        atomicAdd(&a.counters[4], idle_evals);
     }
 }
 
@@ -972,6 +1002,8 @@ void refine_iteration(Ctx& c, int l, bool recheck) {
     // kFlat mode: 2 linear rig (row-invariant targets), 3 many targets with the 8-byte raster,
     // 1 other flat rigs, 0 general
     const int flat_mode = !flat ? 0 : a.row_inv ? 2 : a.N > 16 ? 3 : 1;
+    if (flat_mode && (c.W > (1 << 20) || c.H > (1 << 20)))
+        throw Error(LFDG_INVALID_PARAMS, "refinement supports images up to 2^20 pixels wide / high");
     const size_t smem = 4 * warp_smem_bytes(a.N, flat_mode);
     // the per-warp target tables grow with the number of matching views: ~190 for kFlat, ~150 in
     // general fit the 227 KB of shared memory of a CTA

@@ -303,12 +303,12 @@ __device__ int block_compact(int levels, int* list, int* s_cnt, Pred keep) {
 // hypotheses into a shared tile, then one thread per hypothesis folds the tile row in member
 // order — the same sequential FP64 chain, sample by sample, as sweep_cost (sweep.hpp:85-107).
 template <bool kIdR, bool kCanonK>
-__global__ void __launch_bounds__(256) k_sweep(const float4* __restrict__ lab, int W, int H, int nsp, int v0,
+__global__ void __launch_bounds__(256, 4) k_sweep(const float4* __restrict__ lab, int W, int H, int nsp, int v0,
                                                const Cam* __restrict__ cams, const int* __restrict__ targets,
                                                int n_targets, const int32_t* __restrict__ moff,
                                                const int32_t* __restrict__ mpix, int levels, double inv_lo,
-                                               double inv_hi, double step, float T, uint64_t seed,
-                                               double4* planes) {
+                                               double inv_hi, double step, float T, uint64_t seed, int gw,
+                                               int n_views, double4* planes) {
     extern __shared__ __align__(16) unsigned char smem[];
     // [staging / tile union][cams][s_d][s_P][list]
     constexpr size_t kUnion = kSweepCap * (sizeof(double2) + sizeof(float4)) > kGroup * kTilePitch * sizeof(float)
@@ -326,8 +326,15 @@ __global__ void __launch_bounds__(256) k_sweep(const float4* __restrict__ lab, i
     __shared__ double g_d[kGroup], g_z[kGroup], g_rz[kGroup], g_kz0[kGroup], g_kz1[kGroup];
     __shared__ int g_h[kGroup];
 
-    const int sp = blockIdx.x;
-    const int view = v0 + blockIdx.y;
+    // CTA order (superpixel row, view, superpixel column): the CTAs resident at any time sweep the
+    // same band of image rows in every view, so the target-image rows they gather (the epipolar
+    // band of a rectified rig) stay L2-resident across source views instead of every view
+    // re-streaming its targets from HBM.
+    const int row_tasks = n_views * gw;
+    const int grow = blockIdx.x / row_tasks;
+    const int rem = blockIdx.x - grow * row_tasks;
+    const int sp = grow * gw + rem % gw;
+    const int view = v0 + rem / gw;
     const size_t hw = (size_t)W * H;
     const int* tg = targets + (size_t)view * n_targets;
     for (int i = threadIdx.x; i < n_targets + 1; i += blockDim.x) s_cam[i] = cams[i == 0 ? view : tg[i - 1]];
@@ -549,12 +556,12 @@ void sweep_views(Ctx& c, int v0, int n, const lfdg_sweep_params& p, uint64_t see
     const int threads = 256;
     const size_t smem = std::max(kSweepCap * (sizeof(double2) + sizeof(float4)), kGroup * kTilePitch * sizeof(float)) +
                         (size_t)(nt + 1) * sizeof(Cam) + (size_t)p.levels * (2 * sizeof(double) + sizeof(int));
-    dim3 grid(c.nsp, n);
+    const unsigned grid = (unsigned)c.nsp * (unsigned)n;
     auto launch = [&](auto kernel) {
         LFDG_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         kernel<<<grid, threads, smem, c.stream>>>(c.lab.p, c.W, c.H, c.nsp, v0, c.d_cams.p, d_tg.p, nt, c.moff.p,
-                                                  c.mpix.p, p.levels, inv_lo, inv_hi, step, p.tssd_threshold, seed,
-                                                  c.planes.p);
+                                                  c.mpix.p, p.levels, inv_lo, inv_hi, step, p.tssd_threshold, seed, c.gw,
+                                                  n, c.planes.p);
     };
     if (c.identity_rot && c.canonical_k)
         launch(k_sweep<true, true>);

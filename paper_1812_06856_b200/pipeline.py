@@ -46,6 +46,17 @@ def exchange_views(t, stride: int, n_views: int, world: int, rank: int, group=No
 
     if world == 1:
         return
+    if t.is_cuda and dist.get_backend(group) == "gloo":
+        # gloo moves host memory: stage the device buffer through the host (the CPU-collective
+        # path, e.g. several ranks sharing one GPU in tests); NCCL exchanges in place on the device
+        import torch
+
+        torch.cuda.synchronize(t.device)
+        h = t.cpu()
+        exchange_views(h, stride, n_views, world, rank, group, in_place_allgather)
+        t.copy_(h)
+        torch.cuda.synchronize(t.device)
+        return
     if in_place_allgather and n_views % world == 0:
         chunk = stride * (n_views // world)
         dist.all_gather_into_tensor(t, t[rank * chunk:(rank + 1) * chunk], group=group)
@@ -116,6 +127,8 @@ class HotPath:
         return torch.as_tensor(_CudaArray(ptr, nbytes), device=f"cuda:{self.ctx.device}"), stride
 
     def _allgather(self, which: int):
+        if self.stream is None:
+            self.ctx.synchronize()  # the library's own stream: finish its kernels before torch reads
         t, stride = self._tensor(which)
         exchange_views(t, stride, self.V, self.world, self.rank, self.group)
 

@@ -48,7 +48,7 @@ def main():
         dc.synchronize(); marks["ctx"] = time.time() - t
         for l in range(1, c["iters"] + 1):
             t = time.time()
-            acc, _ = dc.refine_iteration(l)
+            dc.refine_iteration(l, with_stats=False); acc = -1
             dc.rasterize(); dc.synchronize()
             marks[f"refine{l}"] = (round(time.time() - t, 4), acc, dc.refine_work(reset=True))
         print(rep, marks, flush=True)
