@@ -116,7 +116,13 @@ def reference_setup(cfg_name: str, workers: int) -> dict:
 
     c = CONFIGS[cfg_name]
     t0 = time.time()
-    sc = ref.render_scene(c["kind"], c["n_views"], c["width"], c["height"], c["f"], c["baseline"], 0.0, c["grid"])
+    if c.get("rig"):  # a re-aimed rig: the product's renderer (byte-identical to the reference's fixtures)
+        from paper_1812_06856_b200.scenes import render_config
+
+        sc = render_config(cfg_name, gt=True)
+    else:
+        sc = ref.render_scene(c["kind"], c["n_views"], c["width"], c["height"], c["f"], c["baseline"], 0.0,
+                              c["grid"])
     s = ref.Session(sc["lab"], sc["cams"], sc["range"])
     V = sc["lab"].shape[0]
     for v in range(V):
@@ -176,6 +182,18 @@ def reference_sample(st: dict, step: int, workers: int) -> dict:
                 n_refine=n_rf, wall_s=t_slic + t_sw + sum(t_ref))
 
 
+def extrapolator_validation():
+    """The committed check of reference_sample's estimate against full timed reference runs
+    (tools/validate_cpu_extrapolation.py at C1 and C2 on a GPU box's host cores)."""
+    try:
+        rows = [json.loads(x) for x in open(os.path.join(ROOT, "profiles", "r2_cpu_extrapolation.log"))
+                if x.startswith("{")]
+        return {r["config"]: {"full_ms_per_view": r["full_ms_per_view"],
+                              "estimate_over_full": r["estimate_over_full"], "workers": r["workers"]} for r in rows}
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def cpu_cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -208,6 +226,7 @@ def run_reference(args, rank: int, world: int):
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "reference", "sample": sample_desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "reference_detail": {"ms_per_view": ms_view, "setup_s": st["setup_s"],
+                             "extrapolator_validation": extrapolator_validation(),
                              "samples": [{k: v for k, v in x.items()} for x in samples]},
     }
     print(json.dumps(line), flush=True)
@@ -221,8 +240,10 @@ def workload_config(name: str, gpus: int) -> dict:
 
     c = CONFIGS[name]
     V = c["grid"][0] * c["grid"][1] if c["grid"][0] else c["n_views"]
-    return {"workload": f"{name}: cluttered_scene {V} views {c['width']}x{c['height']}"
-                        + (f" ({c['grid'][0]}x{c['grid'][1]} grid rig)" if c["grid"][0] else " (linear rig)")
+    rig = (f" ({c['grid'][0]}x{c['grid'][1]} grid rig)" if c["grid"][0] else
+           " (converging rig: toed-in +-4.2 deg, rolled +-0.5 deg, skewed K)" if c.get("rig") == "converging" else
+           " (linear rig)")
+    return {"workload": f"{name}: cluttered_scene {V} views {c['width']}x{c['height']}" + rig
                         + f", S={c['S']}, L={c['levels']}, {c['iterations']} refine iterations, "
                         + ("all-others matching" if c["max_neighbors"] == 0 else f"{c['max_neighbors']} nearest views"),
             "views": V, "width": c["width"], "height": c["height"], "superpixel_size": c["S"],
@@ -260,7 +281,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     for _ in range(args.warmup):
         hp.run()
     barrier()
-    hp.ctx.refine_work(reset=True)
+    hp.ctx.work_counters(reset=True)
     launches0 = hp.ctx.launch_count()
     sampler = ClockSampler(dev)
     sampler.start()
@@ -291,13 +312,14 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     launches = hp.ctx.launch_count() - launches0
     ms_total = e0.elapsed_time(e1)
     refine_ms = sum(a.elapsed_time(b) for a, b in ev_refine)
-    pix_evals, cand_evals = hp.ctx.refine_work(reset=True)
+    wc = hp.ctx.work_counters(reset=True)
+    pix_evals, cand_evals, sweep_samples = wc["refine_pixel_evals"], wc["refine_candidate_evals"], wc["sweep_samples"]
     t = torch.tensor([ms_total, refine_ms], device=f"cuda:{dev}", dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        pe = torch.tensor([pix_evals], device=f"cuda:{dev}", dtype=torch.float64)
+        pe = torch.tensor([pix_evals, sweep_samples], device=f"cuda:{dev}", dtype=torch.float64)
         dist.all_reduce(pe)
-        pix_evals = int(pe.item())
+        pix_evals, sweep_samples = int(pe[0].item()), int(pe[1].item())
     ms_total, refine_ms = float(t[0]), float(t[1])
     ms_step = ms_total / args.steps
     value = V * args.steps / (ms_total / 1e3)
@@ -372,21 +394,24 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if rank != 0:
         return
     peak = ctypes_fp64_peak(dev)
+    peak32 = ctypes_fp32_peak(dev)
     refine_launches = args.steps * c["iterations"]
     achieved = pix_evals * REFINE_FLOP_PER_PIXEL_EVAL / (refine_ms / 1e3) / 1e12
+    traffic, traffic_note = refine_traffic()
     roofline = {"bound": "fp64", "kernel": "k_refine (refine_iteration)", "achieved": achieved,
                 "peak": peak / 1e12, "unit": "TFLOP/s", "frac": achieved / (peak / 1e12),
                 "peak_source": "measured DFMA stream on this GPU (lfdg_selftest_fp64_peak)",
-                "traffic": refine_traffic(),
+                "traffic": traffic, "traffic_source": traffic_note,
                 "per_launch": {"pixel_evals": pix_evals / refine_launches,
                                "flop": pix_evals * REFINE_FLOP_PER_PIXEL_EVAL / refine_launches,
                                "ms": refine_ms / refine_launches},
                 "share_of_step": refine_ms / ms_total}
+    step_roof = step_roofline(c, V, args.steps, ms_total, pix_evals, sweep_samples, peak, peak32)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step, "ms_per_view": ms_step / V, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": workload_config(args.config, world),
-        "roofline": roofline, "clocks": clocks, "gpu_launches": launches, "e2e": e2e,
+        "roofline": roofline, "step_roofline": step_roof, "clocks": clocks, "gpu_launches": launches, "e2e": e2e,
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.config)
@@ -395,12 +420,73 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
 def refine_traffic():
     """DRAM bytes (read + write) of one k_refine launch from the committed ncu --set full capture
-    (profiles/r1_traffic.json, see profiles/r1_ncu_k_refine.txt); None when absent."""
+    (profiles/r2_traffic.json), used only when that capture was taken of the refine.cu being
+    benched (sha256 recorded beside it); else (None, reason)."""
+    import hashlib
+
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
-            return json.load(f)["k_refine"]["dram_bytes_per_launch"]
+        with open(os.path.join(ROOT, "profiles", "r2_traffic.json")) as f:
+            rec = json.load(f)["k_refine"]
+        src = os.path.join(ROOT, "paper_1812_06856_b200", "csrc", "refine.cu")
+        sha = hashlib.sha256(open(src, "rb").read()).hexdigest()
+        if rec.get("refine_cu_sha256") != sha:
+            return None, "profiles/r2_traffic.json was captured from a different refine.cu"
+        return rec["dram_bytes_per_launch"], f"ncu --set full of this refine.cu ({rec.get('capture', '')})"
     except (OSError, KeyError, ValueError):
-        return None
+        return None, "no committed ncu capture"
+
+
+# Algorithmic work per unit, the step-level roofline's numerators (DESIGN.md §4): a division,
+# square root or exp counts as one operation.
+SWEEP_FP64_PER_SAMPLE = 10   # hx (5), u = hx / z by reciprocal + Markstein (3), fx = u - x0 (1), cost += (1)
+SWEEP_FP32_PER_SAMPLE = 36   # bilinear 27, color_dist2 8, tssd min 1
+SLIC_FP64_PER_CENTRE = 6     # ddx, ddy, ddx^2 + ddy^2 (3), sqrt
+SLIC_FP32_PER_CENTRE = 11    # color_dist2 8, sqrtf, d = dc + w ds (2)
+SLIC_CENTRES = 25            # the +-2 cell window of the assign loop (superpixel.hpp:221-244)
+SLIC_BYTES_PER_PX_ITER = 20  # LAB float4 read + label write
+RAST_BYTES_PER_PX = 8        # label read + depth write (rasterize)
+BUILD_RASTER_BYTES_PER_PX = 24  # label + depth read, 16-byte gather record written
+
+
+def step_roofline(c, V, steps, ms_total, pix_evals, sweep_samples, p64, p32):
+    """Sum over the step's kernels of T_roof,k = max(bytes / HBM, FP64 / P64, FP32 / P32) divided by
+    the measured step time; peaks: HBM from MEASURED_PEAKS.json, FP64 / FP32 measured
+    live by lfdg_selftest_fp64_peak / fp32_peak."""
+    try:
+        hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] * 1e9
+        hbm_src = "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, KeyError, ValueError):
+        hbm, hbm_src = 6.65e12, "fallback 6.65 TB/s (B200_PROFILING.md)"
+    px = V * c["width"] * c["height"]
+    it = c["iterations"]
+    slic_centre_evals = px * 10 * SLIC_CENTRES
+    t = {
+        "k_refine": pix_evals / steps * REFINE_FLOP_PER_PIXEL_EVAL / p64,
+        "k_sweep": max(sweep_samples / steps * SWEEP_FP64_PER_SAMPLE / p64,
+                       sweep_samples / steps * SWEEP_FP32_PER_SAMPLE / p32),
+        "slic": max(slic_centre_evals * SLIC_FP64_PER_CENTRE / p64, slic_centre_evals * SLIC_FP32_PER_CENTRE / p32,
+                    px * 10 * SLIC_BYTES_PER_PX_ITER / hbm),
+        "k_rasterize": (1 + it) * px * RAST_BYTES_PER_PX / hbm,
+        "k_build_raster": it * px * BUILD_RASTER_BYTES_PER_PX / hbm,
+    }
+    t_ms = {k: v * 1e3 for k, v in t.items()}
+    ms_step = ms_total / steps
+    return {"t_roof_ms": t_ms, "sum_t_roof_ms": sum(t_ms.values()), "t_step_ms": ms_step,
+            "frac": sum(t_ms.values()) / ms_step,
+            "counts_per_step": {"refine_pixel_evals": pix_evals / steps, "sweep_samples": sweep_samples / steps,
+                                "slic_centre_tests_bound": slic_centre_evals},
+            "peaks": {"fp64_tflops": p64 / 1e12, "fp32_tflops": p32 / 1e12, "hbm_gbs": hbm / 1e9,
+                      "sources": "fp64/fp32 measured live (DFMA/FFMA streams); " + hbm_src}}
+
+
+def ctypes_fp32_peak(dev: int) -> float:
+    import ctypes
+
+    from paper_1812_06856_b200 import _native as N
+
+    out = ctypes.c_double()
+    N.check(N.lib().lfdg_selftest_fp32_peak(dev, ctypes.byref(out)))
+    return out.value
 
 
 def ctypes_fp64_peak(dev: int) -> float:

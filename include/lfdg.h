@@ -188,9 +188,12 @@ int lfdg_run_refinement(lfdg_ctx* ctx, uint64_t* accepted, uint64_t* violations)
 /* Work counters accumulated by refine_iteration since the last reset: evaluated
  * (candidate, target, member pixel) triples of pair_stats and evaluated candidates. */
 int lfdg_refine_work(lfdg_ctx* ctx, uint64_t* pixel_evals, uint64_t* candidate_evals, int reset);
-/* Diagnostic: (candidate, target, member pixel) triples executed by idle candidate slots of the
- * refinement kernel (slots of a speculative group with no surviving candidate to evaluate). */
-int lfdg_refine_idle_work(lfdg_ctx* ctx, uint64_t* idle_pixel_evals, int reset);
+/* Work counters of the context (out[8]): [0] accepted and [1] violations of the last
+ * refine_iteration, [2] pair_stats (candidate, target, member pixel) evaluations and [3]
+ * evaluated candidates since the last reset, [4] evaluations executed by idle candidate slots of
+ * the refinement kernel (a speculative group with no surviving candidate), [5] sweep_cost samples
+ * (hypothesis, target, member pixel) evaluated by the pruned sweep.  reset clears [2..7]. */
+int lfdg_work_counters(lfdg_ctx* ctx, uint64_t* out, int reset);
 /* min_neighbor_similarity table of make_refine_context (refine.hpp:71), [nsp] floats. */
 int lfdg_get_min_nb_sim(lfdg_ctx* ctx, int view, float* out);
 
@@ -228,6 +231,11 @@ int lfdg_mark_views_ready(lfdg_ctx* ctx, int v0, int n, int what);
 int lfdg_render_scene(int kind, int n_views, int width, int height, double f, double baseline, double extra,
                       int grid_nx, int grid_ny, int threads, float* lab_out, float* rgb_out, float* gt_out,
                       lfdg_camera* cams_out, double* range_out);
+/* The same scene rendered through n_cams caller-given cameras (replacing the rig; any calibrated
+ * cameras: rotations, skew, off-plane centres).  Outputs as lfdg_render_scene, V = n_cams. */
+int lfdg_render_scene_cams(int kind, int n_views, int width, int height, double f, double baseline, double extra,
+                           const lfdg_camera* cams, int n_cams, int threads, float* lab_out, float* rgb_out,
+                           float* gt_out, double* range_out);
 /* rgb_to_scaled_lab (image.hpp:83-107) over n pixels of [n][3] floats. */
 int lfdg_rgb_to_scaled_lab(int64_t n_pixels, const float* rgb, float* lab);
 /* rgb_to_scaled_lab (image.hpp:97-107) on the GPU for n host pixels ([n][3] in, [n][3] out). */
@@ -251,6 +259,8 @@ int lfdg_selftest_expf(int device, const float* in, float* out, size_t n);
 int lfdg_selftest_exp_nonpos(int device, const double* in, double* out, size_t n);
 /* Measured FP64 FMA throughput of the device (FLOP/s, DFMA = 2), the sweep/refine roofline. */
 int lfdg_selftest_fp64_peak(int device, double* flops);
+/* Measured FP32 FFMA throughput of the device (FLOP/s), the FP32 roofline denominator. */
+int lfdg_selftest_fp32_peak(int device, double* flops);
 
 /* ---- out-of-bounds-write detector (guard.cu) ------------------------------------------ */
 /* With LFDG_GUARD=1 in the environment every device buffer is bracketed by 64 KiB guard zones

@@ -63,8 +63,8 @@ EXPORTED = [
     "lfdg_set_planes", "lfdg_get_planes", "lfdg_rasterize", "lfdg_rasterize_views", "lfdg_get_depth",
     "lfdg_set_depth", "lfdg_make_refine_context", "lfdg_set_refine_views", "lfdg_refine_iteration",
     "lfdg_run_refinement", "lfdg_get_min_nb_sim", "lfdg_device_buffer", "lfdg_mark_views_ready",
-    "lfdg_selftest_exp", "lfdg_selftest_expf", "lfdg_render_scene", "lfdg_rgb_to_scaled_lab",
-    "lfdg_upload_images", "lfdg_download_results", "lfdg_selftest_fp64_peak", "lfdg_refine_work", "lfdg_refine_idle_work", "lfdg_selftest_exp_nonpos",
+    "lfdg_selftest_exp", "lfdg_selftest_expf", "lfdg_render_scene", "lfdg_render_scene_cams", "lfdg_rgb_to_scaled_lab",
+    "lfdg_upload_images", "lfdg_download_results", "lfdg_selftest_fp64_peak", "lfdg_selftest_fp32_peak", "lfdg_refine_work", "lfdg_work_counters", "lfdg_selftest_exp_nonpos",
     "lfdg_fuse_views", "lfdg_get_fused", "lfdg_gather_candidates", "lfdg_stability_fuse", "lfdg_upload_rgb",
     "lfdg_rgb_to_scaled_lab_gpu", "lfdg_eval_bad_pixel", "lfdg_debug_guard_enabled", "lfdg_debug_check_guards",
     "lfdg_debug_guard_selftest", "lfdg_upload_rgb8", "lfdg_prefetch_images", "lfdg_commit_images",
@@ -143,6 +143,7 @@ def lib():
         "lfdg_selftest_exp": (I, [I, P, P, C.c_size_t]),
         "lfdg_selftest_expf": (I, [I, P, P, C.c_size_t]),
         "lfdg_render_scene": (I, [I, I, I, I, D, D, D, I, I, I, P, P, P, P, P]),
+        "lfdg_render_scene_cams": (I, [I, I, I, I, D, D, D, P, I, I, P, P, P, P]),
         "lfdg_rgb_to_scaled_lab": (I, [C.c_int64, P, P]),
         "lfdg_upload_images": (I, [P, I, I, P]),
         "lfdg_upload_rgb": (I, [P, I, I, P]),
@@ -150,8 +151,9 @@ def lib():
         "lfdg_rgb_to_scaled_lab_gpu": (I, [I, P, P, C.c_size_t]),
         "lfdg_download_results": (I, [P, I, I, P, P, I]),
         "lfdg_selftest_fp64_peak": (I, [I, C.POINTER(D)]),
+        "lfdg_selftest_fp32_peak": (I, [I, C.POINTER(D)]),
         "lfdg_refine_work": (I, [P, PU64, PU64, I]),
-        "lfdg_refine_idle_work": (I, [P, PU64, I]),
+        "lfdg_work_counters": (I, [P, P, I]),
         "lfdg_selftest_exp_nonpos": (I, [I, P, P, C.c_size_t]),
         "lfdg_fuse_views": (I, [P, I, I, D]),
         "lfdg_get_fused": (I, [P, I, P]),

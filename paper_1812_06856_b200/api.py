@@ -366,11 +366,13 @@ class DeviceContext:
         N.check(self.L.lfdg_refine_work(self.h, C.byref(a), C.byref(b), int(reset)))
         return a.value, b.value
 
-    def refine_idle_work(self, reset: bool = True) -> int:
-        """Pixel-evaluations executed by idle candidate slots (diagnostic)."""
-        a = C.c_uint64()
-        N.check(self.L.lfdg_refine_idle_work(self.h, C.byref(a), int(reset)))
-        return a.value
+    def work_counters(self, reset: bool = False) -> dict:
+        """The context's work counters (lfdg_work_counters); reset clears the accumulating ones."""
+        out = np.zeros(8, np.uint64)
+        N.check(self.L.lfdg_work_counters(self.h, N.ptr(out), int(reset)))
+        return {"accepted": int(out[0]), "violations": int(out[1]), "refine_pixel_evals": int(out[2]),
+                "refine_candidate_evals": int(out[3]), "refine_idle_slot_evals": int(out[4]),
+                "sweep_samples": int(out[5])}
 
     # -- fusion (fusion.hpp:31-100)
     def fuse_views(self, epsilon: float, v0: int = 0, n: Optional[int] = None):

@@ -398,15 +398,16 @@ int lfdg_run_refinement(lfdg_ctx* p, uint64_t* accepted, uint64_t* violations) {
     });
 }
 
-int lfdg_refine_idle_work(lfdg_ctx* p, uint64_t* idle_pixel_evals, int reset) {
+int lfdg_work_counters(lfdg_ctx* p, uint64_t* out, int reset) {
     return guarded([&] {
         auto* c = C(p);
         activate(c);
-        unsigned long long h = 0;
-        LFDG_CUDA_CHECK(cudaMemcpyAsync(&h, c->counters.p + 4, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+        if (!out) throw lfdg::Error(LFDG_STATE, "null output");
+        unsigned long long h[8];
+        LFDG_CUDA_CHECK(cudaMemcpyAsync(h, c->counters.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
         LFDG_CUDA_CHECK(cudaStreamSynchronize(c->stream));
-        if (idle_pixel_evals) *idle_pixel_evals = h;
-        if (reset) LFDG_CUDA_CHECK(cudaMemsetAsync(c->counters.p + 4, 0, sizeof(unsigned long long), c->stream));
+        for (int i = 0; i < 8; ++i) out[i] = h[i];
+        if (reset) LFDG_CUDA_CHECK(cudaMemsetAsync(c->counters.p + 2, 0, 6 * sizeof(unsigned long long), c->stream));
     });
 }
 

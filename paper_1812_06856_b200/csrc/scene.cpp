@@ -357,9 +357,9 @@ extern "C" {
 // Scene kinds as in oracle/ref_harness.cpp: 0 cluttered, 1 staircase, 2 wall(depth = extra),
 // 3 slanted(tilt = extra), 4 occluder; grid_nx > 0 replaces the rig by make_grid_rig.
 // Outputs (any may be NULL): lab/rgb [V][H][W][3], gt [V][H][W], cameras [V], range[2].
-int lfdg_render_scene(int kind, int n_views, int width, int height, double f, double baseline, double extra,
-                      int grid_nx, int grid_ny, int threads, float* lab_out, float* rgb_out, float* gt_out,
-                      lfdg_camera* cams_out, double* range_out) {
+static int render_impl(int kind, int n_views, int width, int height, double f, double baseline, double extra,
+                       int grid_nx, int grid_ny, const lfdg_camera* cams_in, int n_cams_in, int threads,
+                       float* lab_out, float* rgb_out, float* gt_out, lfdg_camera* cams_out, double* range_out) {
     if (width < 1 || height < 1 || n_views < 1) return LFDG_INVALID_PARAMS;
     Scene s;
     switch (kind) {
@@ -371,9 +371,16 @@ int lfdg_render_scene(int kind, int n_views, int width, int height, double f, do
         default: return LFDG_INVALID_PARAMS;
     }
     if (grid_nx > 0) s.cams = grid_rig(grid_nx, grid_ny, f, baseline, width, height);
+    if (cams_in) s.cams.assign(cams_in, cams_in + n_cams_in);  // the scene under caller-given cameras
     if (s.cams.size() < 2) return LFDG_INVARIANT;  // SceneSpec::validate (fixtures.hpp:74)
     const int V = static_cast<int>(s.cams.size());
     const size_t hw = static_cast<size_t>(width) * height;
+    if (cams_out) std::memcpy(cams_out, s.cams.data(), V * sizeof(lfdg_camera));
+    if (range_out) {
+        range_out[0] = s.dmin;
+        range_out[1] = s.dmax;
+    }
+    if (!lab_out && !rgb_out && !gt_out) return LFDG_OK;  // rig and range only
     std::vector<float> rgb_tmp;
     float* rgb = rgb_out;
     if (!rgb) {
@@ -394,12 +401,25 @@ int lfdg_render_scene(int kind, int n_views, int width, int height, double f, do
                 to_lab(rgb + 3 * i, lab_out + 3 * i);
         });
     }
-    if (cams_out) std::memcpy(cams_out, s.cams.data(), V * sizeof(lfdg_camera));
-    if (range_out) {
-        range_out[0] = s.dmin;
-        range_out[1] = s.dmax;
-    }
     return LFDG_OK;
+}
+
+int lfdg_render_scene(int kind, int n_views, int width, int height, double f, double baseline, double extra,
+                      int grid_nx, int grid_ny, int threads, float* lab_out, float* rgb_out, float* gt_out,
+                      lfdg_camera* cams_out, double* range_out) {
+    return render_impl(kind, n_views, width, height, f, baseline, extra, grid_nx, grid_ny, nullptr, 0, threads, lab_out,
+                       rgb_out, gt_out, cams_out, range_out);
+}
+
+// The scene of (kind, n_views, W, H, f, baseline, extra) rendered through caller-given cameras
+// (any calibrated rig: rotations, skew, off-plane centres) — render_scene with spec.cameras
+// replaced, as tests/acceptance.cpp:398-399 does with make_grid_rig.
+int lfdg_render_scene_cams(int kind, int n_views, int width, int height, double f, double baseline, double extra,
+                           const lfdg_camera* cams, int n_cams, int threads, float* lab_out, float* rgb_out,
+                           float* gt_out, double* range_out) {
+    if (!cams || n_cams < 2) return LFDG_INVALID_PARAMS;
+    return render_impl(kind, n_views, width, height, f, baseline, extra, 0, 0, cams, n_cams, threads, lab_out, rgb_out,
+                       gt_out, nullptr, range_out);
 }
 
 // rgb_to_scaled_lab over n pixels (image.hpp:97-107).

@@ -58,6 +58,59 @@ __global__ void k_dfma(double* out, int iters, double a, double b) {
 }
 }  // namespace
 
+namespace {
+__global__ void k_ffma(float* out, int iters, float a, float b) {
+    float x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+    for (int i = 0; i < iters; ++i) {
+        x0 = __fmaf_rn(x0, a, b); x1 = __fmaf_rn(x1, a, b); x2 = __fmaf_rn(x2, a, b); x3 = __fmaf_rn(x3, a, b);
+        x4 = __fmaf_rn(x4, a, b); x5 = __fmaf_rn(x5, a, b); x6 = __fmaf_rn(x6, a, b); x7 = __fmaf_rn(x7, a, b);
+    }
+    const float s = ((x0 + x1) + (x2 + x3)) + ((x4 + x5) + (x6 + x7));
+    if (s == 1.2345f) out[0] = s;
+}
+
+// Best-of-5 event time of `launch` over `flop` floating-point operations -> FLOP/s.
+template <typename L>
+double time_flops(L launch, double flop) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    launch();  // warm-up
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        cudaEventRecord(e0);
+        launch();
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        best = ms < best ? ms : best;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return flop / (best * 1e-3);
+}
+}  // namespace
+
+// FP32 roofline denominator (the sweep's bilinear / TSSD arithmetic): FFMA stream, 8 independent
+// chains per thread, 148 SMs x 8 CTAs x 256 threads; an FFMA counts as 2 FLOP.
+extern "C" int lfdg_selftest_fp32_peak(int device, double* flops) {
+    try {
+        LFDG_CUDA_CHECK(cudaSetDevice(device));
+        int sms = 0;
+        LFDG_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        lfdg::DevBuf<float> out;
+        out.alloc(1);
+        const int iters = 16384, blocks = sms * 8, threads = 256;
+        *flops = time_flops([&] { k_ffma<<<blocks, threads>>>(out.p, iters, 0.999999f, 1e-7f); },
+                            2.0 * 8.0 * iters * (double)blocks * threads);
+        LFDG_CUDA_CHECK(cudaGetLastError());
+        return LFDG_OK;
+    } catch (const lfdg::Error& e) {
+        return e.code;
+    }
+}
+
 extern "C" int lfdg_selftest_fp64_peak(int device, double* flops) {
     try {
         LFDG_CUDA_CHECK(cudaSetDevice(device));

@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(256, 4) k_sweep(const float4* __restrict__ lab
                                                int n_targets, const int32_t* __restrict__ moff,
                                                const int32_t* __restrict__ mpix, int levels, double inv_lo,
                                                double inv_hi, double step, float T, uint64_t seed, int gw,
-                                               int n_views, double4* planes) {
+                                               int n_views, double4* planes, unsigned long long* samples) {
     extern __shared__ __align__(16) unsigned char smem[];
     // [staging / tile union][cams][s_d][s_P][list]
     constexpr size_t kUnion = kSweepCap * (sizeof(double2) + sizeof(float4)) > kGroup * kTilePitch * sizeof(float)
@@ -395,8 +395,10 @@ __global__ void __launch_bounds__(256, 4) k_sweep(const float4* __restrict__ lab
 
     // Continue the chains of list[0, cnt) over targets [t_begin, n_targets), pruning after
     // each target (prune: keep only partial cost <= B).  Returns the surviving count.
+    unsigned long long n_samples = n_targets > 0 ? (unsigned long long)levels * n : 0;  // phase A
     auto advance = [&](int cnt, int t_begin, bool prune, double B) -> int {
         for (int ti = t_begin; ti < n_targets && cnt > 0; ++ti) {
+            n_samples += (unsigned long long)cnt * n;
             const Cam& tc = s_cam[ti + 1];
             const float4* timg = lab + (size_t)tg[ti] * hw;
             for (int g0 = 0; g0 < cnt; g0 += kGroup) {
@@ -478,7 +480,10 @@ __global__ void __launch_bounds__(256, 4) k_sweep(const float4* __restrict__ lab
         __syncthreads();
         best = block_argmin(s_P, s_d, s_list, cnt + 1, red_c, red_d, red_k);
     }
-    if (threadIdx.x == 0) planes[(size_t)view * nsp + sp] = make_double4(s_d[best], 0.0, 0.0, -1.0);
+    if (threadIdx.x == 0) {
+        planes[(size_t)view * nsp + sp] = make_double4(s_d[best], 0.0, 0.0, -1.0);
+        atomicAdd(samples, n_samples);  // work counter [5]: samples of this superpixel's sweep
+    }
 }
 
 // rasterize (sweep.hpp:44-63), one thread per pixel of views [v0, v0+n).
@@ -561,7 +566,7 @@ void sweep_views(Ctx& c, int v0, int n, const lfdg_sweep_params& p, uint64_t see
         LFDG_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         kernel<<<grid, threads, smem, c.stream>>>(c.lab.p, c.W, c.H, c.nsp, v0, c.d_cams.p, d_tg.p, nt, c.moff.p,
                                                   c.mpix.p, p.levels, inv_lo, inv_hi, step, p.tssd_threshold, seed, c.gw,
-                                                  n, c.planes.p);
+                                                  n, c.planes.p, c.counters.p + 5);
     };
     if (c.identity_rot && c.canonical_k)
         launch(k_sweep<true, true>);

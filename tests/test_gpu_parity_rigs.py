@@ -4,7 +4,9 @@
 * ``tz``      identity rotations, canonical K, cameras at different depths: kIdR + kCanonK, not kFlat;
 * ``rot``     small per-view rotations, canonical K: the general-R paths;
 * ``skew``    identity rotations, K01 != 0: the general-K paths (rays depend on both coordinates);
-* ``general`` rotations + skew + t.z: nothing specialised.
+* ``general`` rotations + skew + t.z: nothing specialised;
+* ``converging`` the bench's C3G rig at small size (toed-in, rolled, skewed cameras) with images
+  rendered through those cameras (lfdg_render_scene_cams), so the geometry is self-consistent.
 
 Images come from the rectified renderer; the perturbed cameras are valid PinholeCameras
 (orthonormal R, upper-triangular K with K22 = 1) but do not match the pixels, which is irrelevant
@@ -46,12 +48,16 @@ def _cams(kind, base):
     return cams
 
 
-@pytest.fixture(scope="module", params=["grid", "tz", "rot", "skew", "general"])
+@pytest.fixture(scope="module", params=["grid", "tz", "rot", "skew", "general", "converging"])
 def rig(request, ref):
-    from paper_1812_06856_b200 import api
+    from paper_1812_06856_b200 import api, scenes
 
     kind = request.param
-    if kind == "grid":
+    if kind == "converging":
+        base = scenes.render_scene("cluttered", 4, W, H, 160.0, 0.1, gt=False, lab=False)
+        cams = scenes.converging_rig(base["cams"], base["range"])
+        sc = scenes.render_scene_cams("cluttered", 4, W, H, 160.0, 0.1, cams)
+    elif kind == "grid":
         sc = ref.render_scene("cluttered", 0, W, H, 160.0, 0.1, grid=(2, 2))
         cams = sc["cams"]
     else:

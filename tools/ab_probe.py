@@ -68,11 +68,13 @@ def main():
             out[b] = round(ev[a].elapsed_time(ev[b]), 2)
         out["refine_total"] = round(sum(v for k, v in out.items() if k.startswith("refine")), 2)
         out["total"] = round(ev[keys[0]].elapsed_time(ev[keys[-1]]), 2)
-        pe, ce = dc.refine_work(reset=True)
+        pe, ce = dc.refine_work(reset=False)
         out["pix_evals_2reps"] = pe
         out["cand_evals_2reps"] = ce
-        if hasattr(dc, "refine_idle_work"):
-            out["idle_pix_evals_2reps"] = dc.refine_idle_work(reset=True)
+        if hasattr(dc, "work_counters"):
+            wc = dc.work_counters(reset=True)
+            out["idle_pix_evals_2reps"] = wc["refine_idle_slot_evals"]
+            out["sweep_samples_2reps"] = wc["sweep_samples"]
         planes = np.stack([dc.get_planes(v) for v in range(V)])
         if ref_planes is None:
             ref_planes = planes
