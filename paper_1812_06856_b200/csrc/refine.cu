@@ -627,7 +627,7 @@ __global__ void __launch_bounds__(128, refine_min_blocks(kFlat))
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int gwarp = blockIdx.x * 4 + warp;
+    const int gwarp = blockIdx.x * (blockDim.x >> 5) + warp;
     unsigned char* base = smem_raw + warp * warp_smem_bytes(a.N, kFlat);
     WarpSmem w;
     w.cw = cache_width(a.N, kFlat);
@@ -1004,9 +1004,11 @@ void refine_iteration(Ctx& c, int l, bool recheck) {
     const int flat_mode = !flat ? 0 : a.row_inv ? 2 : a.N > 16 ? 3 : 1;
     if (flat_mode && (c.W > (1 << 20) || c.H > (1 << 20)))
         throw Error(LFDG_INVALID_PARAMS, "refinement supports images up to 2^20 pixels wide / high");
-    const size_t smem = 4 * warp_smem_bytes(a.N, flat_mode);
-    // the per-warp target tables grow with the number of matching views: ~190 for kFlat, ~150 in
-    // general fit the 227 KB of shared memory of a CTA
+    // four warps per CTA; fewer when the per-warp tables (which grow with the number of matching
+    // views) would not fit the 227 KB of shared memory of a CTA — one warp holds ~1000 targets
+    const size_t wbytes = warp_smem_bytes(a.N, flat_mode);
+    const int warps = 4 * wbytes <= 227 * 1024 ? 4 : 2 * wbytes <= 227 * 1024 ? 2 : 1;
+    const size_t smem = warps * wbytes;
     if (smem > 227 * 1024) throw Error(LFDG_INVALID_PARAMS, "too many matching views for the refinement kernel");
     if (rn > 0) {
         // the refine gather raster from the current snapshot (labels, depth)
@@ -1023,16 +1025,17 @@ void refine_iteration(Ctx& c, int l, bool recheck) {
         auto launch = [&](auto kernel) {
             LFDG_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             int per_sm = 0;
-            LFDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 128, smem));
+            LFDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 32 * warps, smem));
             const int n_tasks = rn * c.nsp;
-            const int blocks = std::max(1, std::min(per_sm * c.sm_count, (n_tasks + 3) / 4));
+            const int blocks = std::max(1, std::min(per_sm * c.sm_count, (n_tasks + warps - 1) / warps));
             RefineScratch& rd = c.refine_s;
             rd.task_counter.alloc(1);
-            rd.cand.alloc((size_t)blocks * 4 * cap);
-            rd.es.alloc((size_t)blocks * 4 * cap);
-            rd.acc.alloc((size_t)blocks * 4 * cap);
+            rd.cand.alloc((size_t)blocks * warps * cap);
+            rd.es.alloc((size_t)blocks * warps * cap);
+            rd.acc.alloc((size_t)blocks * warps * cap);
             LFDG_CUDA_CHECK(cudaMemsetAsync(rd.task_counter.p, 0, sizeof(int), c.stream));
-            kernel<<<blocks, 128, smem, c.stream>>>(a, n_tasks, rd.task_counter.p, cap, rd.cand.p, rd.es.p, rd.acc.p);
+            kernel<<<blocks, 32 * warps, smem, c.stream>>>(a, n_tasks, rd.task_counter.p, cap, rd.cand.p, rd.es.p,
+                                                          rd.acc.p);
         };
         // kFlat (flat above): every rotation I, canonical and identical K, every camera centre at
         // z = 0 (then every rel_trans.z = 0): the rectified / grid rigs of the fixtures.

@@ -538,8 +538,9 @@ std::vector<int> matching_views(const Ctx& c, int view, int max_neighbors) {
 
 void sweep_views(Ctx& c, int v0, int n, const lfdg_sweep_params& p, uint64_t seed) {
     if (p.levels < 2) throw Error(LFDG_INVALID_PARAMS, "sweep levels must be >= 2");
-    // the hypotheses of one superpixel live in shared memory (and the prune list in the tile)
-    if (p.levels > 4096) throw Error(LFDG_INVALID_PARAMS, "sweep levels > 4096 are not supported");
+    // the hypotheses of one superpixel live in shared memory (and the prune list in the tile,
+    // kGroup * kTilePitch ints): up to 8192 levels
+    if (p.levels > 8192) throw Error(LFDG_INVALID_PARAMS, "sweep levels > 8192 are not supported");
     if (!(p.tssd_threshold > 0)) throw Error(LFDG_INVALID_PARAMS, "tssd threshold must be > 0");
     if (!(0 < c.d_min && c.d_min < c.d_max)) throw Error(LFDG_INVARIANT, "depth range requires 0 < d_min < d_max");
     if (v0 < 0 || n < 0 || v0 + n > c.V) throw Error(LFDG_STATE, "view range out of bounds");

@@ -148,3 +148,53 @@ def test_many_matching_views(ref, grid):
     for v in range(nv):
         assert np.array_equal(dc.get_planes(v), rs.planes(v)), f"refine view {v}"
     assert acc_g == acc_r
+
+
+def test_hundreds_of_matching_views(ref):
+    """Inputs the reference accepts at any size: 320 views (N = 319 matching views, off-plane
+    camera centres so the general refine kernel runs with its per-target tables; shared memory
+    then holds two warps per CTA instead of four) and 5000 sweep levels.  Sampled sweep winners and
+    refine tasks are compared with the reference."""
+    from paper_1812_06856_b200 import api
+
+    V, w, h = 320, 48, 36
+    sc = ref.render_scene("cluttered", V, w, h, 48.0, 0.002)
+    cams = sc["cams"].copy()
+    cams[:, 20] = 0.001 * np.arange(V)  # t.z != 0: not kFlat
+    rs = ref.Session(sc["lab"], cams, sc["range"])
+    dc = api.DeviceContext(0)
+    dc.set_views(sc["lab"], cams, sc["range"])
+    dc.slic_views(0, V, api.SlicParams(12, 0.1, 10))
+    for v in range(V):
+        rs.set_grid_from_labels(v, dc.get_grid(v).label_map, 12)
+    for v in (0, 7):
+        rs.slic(v, 12, 0.1, 10)
+        assert np.array_equal(dc.get_grid(v).label_map, rs.grid(v)["labels"])
+    dc.sweep_views(0, V, api.SweepParams(4, 0.05, 0), 0)
+    want = rs.sweep_sample(5, np.arange(12, dtype=np.int32), 4, 0.05, 0, 0)
+    assert np.array_equal(dc.get_planes(5), want)
+    for v in range(V):
+        rs.set_planes(v, dc.get_planes(v))
+    rs.rasterize()
+    dc.rasterize()
+    rs.refine_context(4, iterations=1, size_init=24)
+    dc.make_refine_context(api.EnergyParams(iterations=1, size_init=24), 4)
+    rng = np.random.default_rng(3)
+    tv = rng.integers(0, V, 200)
+    ts = rng.integers(0, 12, 200)
+    want, _ = rs.refine_tasks(1, tv, ts)
+    dc.refine_iteration(1, with_stats=False)
+    got = np.stack([dc.get_planes(int(v))[int(s)] for v, s in zip(tv, ts)])
+    assert np.array_equal(got, want)
+    # 5000 sweep levels (the reference accepts any L >= 2)
+    dc2 = api.DeviceContext(0)
+    sc2 = ref.render_scene("cluttered", 3, 64, 48, 64.0, 0.1)
+    rs2 = ref.Session(sc2["lab"], sc2["cams"], sc2["range"])
+    dc2.set_views(sc2["lab"], sc2["cams"], sc2["range"])
+    dc2.slic(0, api.SlicParams(12, 0.1, 10))
+    rs2.slic(0, 12, 0.1, 10)
+    for v in (1, 2):
+        dc2.slic(v, api.SlicParams(12, 0.1, 10))
+        rs2.slic(v, 12, 0.1, 10)
+    got = dc2.sweep(0, api.SweepParams(5000, 0.05, 0), 3)
+    assert np.array_equal(got, rs2.sweep(0, 5000, 0.05, 0, 3))
