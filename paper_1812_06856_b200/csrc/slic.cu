@@ -149,10 +149,12 @@ __global__ void __launch_bounds__(256) k_slic_update(const float4* __restrict__ 
     const int xa = max(0, bx[0]), xb = min(W, 1 - bx[2]);
     const int ya = max(0, bx[1]), yb = min(H, 1 - bx[3]);
     // colour sums: lane k < 3 owns channel k's sequential sum; each step's member colours are
-    // staged in shared memory and added in ascending lane (= row-major pixel) order
-    __shared__ float4 s_col[8][32];
-    float4* buf = s_col[(threadIdx.x >> 5) & 7];
-    const float* bch = reinterpret_cast<const float*>(buf) + (lane < 3 ? lane : 0);
+    // converted to double by the member lanes (all 32 at once: the conversion unit is the
+    // kernel's bottleneck when three lanes convert member by member), staged in shared memory and
+    // added in ascending lane (= row-major pixel) order
+    __shared__ double4 s_col[8][32];
+    double4* buf = s_col[(threadIdx.x >> 5) & 7];
+    const double* bch = reinterpret_cast<const double*>(buf) + (lane < 3 ? lane : 0);
     long long sx = 0, sy = 0;
     int cnt = 0;
     double sc = 0;  // this lane's channel sum (lanes 0-2)
@@ -193,7 +195,7 @@ __global__ void __launch_bounds__(256) k_slic_update(const float4* __restrict__ 
             const bool m = lv == id;
             unsigned mask = __ballot_sync(LFDG_FULL_MASK, m);
             if (!mask) continue;
-            if (m) buf[lane] = cv;
+            if (m) buf[lane] = make_double4((double)cv.x, (double)cv.y, (double)cv.z, 0.0);
             const int n = __popc(mask);
             sx += __reduce_add_sync(LFDG_FULL_MASK, m ? (unsigned)x : 0u);
             sy += (long long)y * n;
@@ -203,7 +205,7 @@ __global__ void __launch_bounds__(256) k_slic_update(const float4* __restrict__ 
                 while (mask) {
                     const int j = __ffs(mask) - 1;
                     mask &= mask - 1;
-                    sc += (double)bch[4 * j];
+                    sc += bch[4 * j];
                 }
             }
             __syncwarp();
