@@ -620,7 +620,12 @@ __device__ __forceinline__ unsigned recheck_acceptances(const RefineArgs& a, con
 #ifndef LFDG_REFINE_MINB
 #define LFDG_REFINE_MINB 8
 #endif
-__host__ __device__ constexpr int refine_min_blocks(int flat_mode) { return flat_mode == 3 ? 7 : LFDG_REFINE_MINB; }
+#ifndef LFDG_REFINE_MINB_GENERAL
+#define LFDG_REFINE_MINB_GENERAL 8
+#endif
+__host__ __device__ constexpr int refine_min_blocks(int flat_mode) {
+    return flat_mode == 3 ? 7 : flat_mode == 0 ? LFDG_REFINE_MINB_GENERAL : LFDG_REFINE_MINB;
+}
 template <bool kIdR, bool kCanonK, int kFlat, bool kRecheck>
 __global__ void __launch_bounds__(128, refine_min_blocks(kFlat))
     k_refine(RefineArgs a, int n_tasks, int* task_counter, int cap, double4* g_cand, double* g_es, int2* g_acc) {
