@@ -252,6 +252,19 @@ def workload_config(name: str, gpus: int) -> dict:
             "l2_policy": "inputs larger than L2 (LAB images alone are V x 33 MB)"}
 
 
+def _all_reduce(t, op=None):
+    """all_reduce that also works on a gloo group (host copy of a device tensor)."""
+    import torch.distributed as dist
+
+    op = dist.ReduceOp.SUM if op is None else op
+    if t.is_cuda and dist.get_backend() == "gloo":
+        h = t.cpu()
+        dist.all_reduce(h, op=op)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=op)
+
+
 def run_ours(args, rank: int, world: int, local_rank: int):
     import torch
     import torch.distributed as dist
@@ -261,7 +274,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     from paper_1812_06856_b200.api import EnergyParams, SlicParams, SweepParams
     from paper_1812_06856_b200.pipeline import HotPath, HotPathConfig
 
-    dev = local_rank
+    dev = local_rank % max(1, torch.cuda.device_count())
     torch.cuda.set_device(dev)
     c = scenes.CONFIGS[args.config]
     threads = max(1, cpu_cores() // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world))))
@@ -316,9 +329,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     pix_evals, cand_evals, sweep_samples = wc["refine_pixel_evals"], wc["refine_candidate_evals"], wc["sweep_samples"]
     t = torch.tensor([ms_total, refine_ms], device=f"cuda:{dev}", dtype=torch.float64)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        _all_reduce(t, op=dist.ReduceOp.MAX)
         pe = torch.tensor([pix_evals, sweep_samples], device=f"cuda:{dev}", dtype=torch.float64)
-        dist.all_reduce(pe)
+        _all_reduce(pe)
         pix_evals, sweep_samples = int(pe[0].item()), int(pe[1].item())
     ms_total, refine_ms = float(t[0]), float(t[1])
     ms_step = ms_total / args.steps
@@ -345,7 +358,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         torch.cuda.synchronize()
         te = torch.tensor([f0.elapsed_time(f1)], device=f"cuda:{dev}", dtype=torch.float64)
         if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            _all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": V * args.steps / (float(te[0]) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(host_imgs.nbytes),
                "d2h_bytes_per_step": int(planes_pin.nbytes + depth_pin.nbytes) * world,
@@ -368,7 +381,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         torch.cuda.synchronize()
         te = torch.tensor([f0.elapsed_time(f1)], device=f"cuda:{dev}", dtype=torch.float64)
         if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            _all_reduce(te, op=dist.ReduceOp.MAX)
         e2e["pipelined"] = {"value": V * args.steps / (float(te[0]) / 1e3), "unit": UNIT,
                             "h2d_bytes_per_step": int(host_imgs.nbytes),
                             "d2h_bytes_per_step": int(planes_pin.nbytes + depth_pin.nbytes) * world,
@@ -387,7 +400,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         torch.cuda.synchronize()
         te = torch.tensor([f0.elapsed_time(f1)], device=f"cuda:{dev}", dtype=torch.float64)
         if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            _all_reduce(te, op=dist.ReduceOp.MAX)
         e2e["from_srgb"] = {"value": V * args.steps / (float(te[0]) / 1e3), "unit": UNIT,
                             "h2d_bytes_per_step": int(host_imgs.nbytes), "ms_per_step": float(te[0]) / args.steps}
 
@@ -547,8 +560,15 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        # NCCL over NVLink; LFDG_BENCH_BACKEND=gloo runs the same ranks through host collectives
+        # (tests: several ranks sharing one GPU, where NCCL refuses duplicate devices)
+        backend = os.environ.get("LFDG_BENCH_BACKEND", "nccl")
+        dev = local_rank % max(1, torch.cuda.device_count())
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
+        else:
+            dist.init_process_group(backend)
     try:
         run_ours(args, rank, world, local_rank)
     finally:

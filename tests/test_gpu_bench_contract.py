@@ -48,3 +48,20 @@ def test_bench_line_reference_arm():
     assert d["value"] > 0 and d["unit"] == "views/s"
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["cpu_baseline"]["kind"] in ("reference", "port")
+
+
+def test_bench_two_ranks_self_launch():
+    """`python bench.py --gpus 2` without a launcher starts its two ranks itself
+    (torch.distributed.run) and rank 0 prints one line with n_gpus 2; both ranks share the test
+    box's one GPU through gloo host collectives (LFDG_BENCH_BACKEND=gloo; NCCL on a real node)."""
+    env = dict(os.environ, LFDG_BENCH_BACKEND="gloo")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "C1", "--gpus", "2",
+                          "--steps", "2", "--warmup", "3", "--no-cpu-baseline"],
+                         capture_output=True, text=True, cwd=ROOT, timeout=900, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["parallelism"] == "view-partition x2"
+    assert d["e2e"]["value"] > 0
