@@ -168,7 +168,10 @@ def lib():
         "lfdg_debug_check_guards": (I, [PU64, PU64]),
         "lfdg_debug_guard_selftest": (I, [I, PU64]),
     }
+    allow_missing = os.environ.get("LFDG_ALLOW_MISSING_SYMBOLS") == "1"  # dev A/B against older builds
     for name, (res, args) in sig.items():
+        if allow_missing and not hasattr(L, name):
+            continue
         fn = getattr(L, name)
         fn.restype = res
         fn.argtypes = args

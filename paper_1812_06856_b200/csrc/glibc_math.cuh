@@ -222,8 +222,11 @@ LFDG_HD double exp_nonpos(double x) {
 __device__ __forceinline__ bool exp_nonpos_in_core(double x) {
     return (unsigned)__double2hiint(x) - 0xBC900000u < 0x03F00000u;  // hi in [hi(-2^-54), hi(-512))
 }
-__device__ __forceinline__ double exp_nonpos_core(double x) {
-    double kd = fma_(x, LFDG_EXPC(0), LFDG_EXPC(1));
+__device__ __forceinline__ double exp_nonpos_core_kd(double x) { return fma_(x, LFDG_EXPC(0), LFDG_EXPC(1)); }
+// the main path from kd = exp_nonpos_core_kd(x); the result is < 2^((n >> 7) + 1) for
+// n = (int)lo(kd) = round(x 128 / ln 2) (table scale 2^(n/128) < 2^((n >> 7) + 1) / 1.0054, times
+// 1 + tmp with |tmp| < 0.0028)
+__device__ __forceinline__ double exp_nonpos_core_from(double kd, double x) {
     const uint64_t ki = as_u64(kd);
     kd = kd - LFDG_EXPC(1);
     const double r = fma_(kd, LFDG_EXPC(3), fma_(kd, LFDG_EXPC(2), x));
@@ -236,6 +239,7 @@ __device__ __forceinline__ double exp_nonpos_core(double x) {
     const double scale = as_f64(sbits);
     return fma_(scale, tmp, scale);
 }
+__device__ __forceinline__ double exp_nonpos_core(double x) { return exp_nonpos_core_from(exp_nonpos_core_kd(x), x); }
 #endif
 
 // __expf_fma (glibc sysdeps/ieee754/flt-32/e_expf.c, x86-64 FMA build).

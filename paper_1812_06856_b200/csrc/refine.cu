@@ -92,6 +92,16 @@ __device__ __forceinline__ double exp_vis(double x) {
     return libm::exp_nonpos_in_core(x) ? libm::exp_nonpos_core(x) : exp_vis_slow(x);
 }
 
+// vis_sum += exp(x) (refine.hpp:158, x <= 0): glibc's main path inline when x is in its range
+// (integer test on the high word), exp(x) = +0 for x <= -746 (glibc rounds it to zero; vis_sum + 0
+// = vis_sum for vis_sum >= +0) without a call, the rest of glibc's path out of line.
+__device__ __forceinline__ void accumulate_vis(double& vis_sum, double x) {
+    if (libm::exp_nonpos_in_core(x))
+        vis_sum += libm::exp_nonpos_core(x);
+    else if (!(x <= -746.0))
+        vis_sum += exp_vis_slow(x);
+}
+
 // depth_consistency (refine.hpp:34-37)
 __device__ __forceinline__ double depth_consistency(double d1, double d2, double two_sigma2) {
     const double r = 1.0 / d1 - 1.0 / d2;
@@ -183,13 +193,13 @@ struct TargetFlat {  // kFlat: R = I, t.z = 0 and the shared K make everything b
 // Target-independent part of pair_stats' transfer for one member pixel (refine.hpp:131-137):
 // s v, and for kFlat (every R = I, every t.z = 0, one shared K) z = s, 1/z, K02 z, K12 z and,
 // for a linear rig, the rounded target row.
-struct __align__(16) PixGeo {  // laid out for 16-byte shared loads of the pairs the hot loop reads together
-    double sv0, f_kz0;
-    double f_inv, sv2;
-    double sv1, f_kz1;
+// 56 bytes (a 16-byte-aligned 64-byte layout for paired loads cost the many-target mode (C4) its
+// 7th CTA per SM: +17 % refine time there)
+struct PixGeo {
+    double sv0, sv1, sv2;
+    double f_inv, f_kz0, f_kz1;
     int f_py;
     int ok;
-    int pad[2];
 };
 struct WarpSmem {
     double4* cand;  // [cap]   (global scratch)
@@ -374,7 +384,7 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
                     if (td <= 0) continue;  // no target depth: not in X or Y
                     if (zt <= (double)td * (1.0 + 1e-6)) {
                         const double rr = inv_z - (kFlat == 3 ? 1.0 / (double)td : __hiloint2double(r.w, r.z));
-                        vis_sum += exp_vis(-rr * rr * a.inv_two_sigma2);
+                        accumulate_vis(vis_sum, -rr * rr * a.inv_two_sigma2);
                         ++x_count;
                     } else {
                         y_nonempty = true;
@@ -425,7 +435,7 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
                     if (td <= 0) continue;  // no target depth: not in X or Y
                     if (zt <= (double)td * (1.0 + 1e-6)) {
                         const double rr = inv_z - __hiloint2double(r.w, r.z);
-                        vis_sum += exp_vis(-rr * rr * a.inv_two_sigma2);
+                        accumulate_vis(vis_sum, -rr * rr * a.inv_two_sigma2);
                         ++x_count;
                     } else {
                         y_nonempty = true;

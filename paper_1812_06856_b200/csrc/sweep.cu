@@ -302,8 +302,18 @@ __device__ int block_compact(int levels, int* list, int* s_cnt, Pred keep) {
 // B and C run member-parallel: each thread samples one member pixel for up to kGroup
 // hypotheses into a shared tile, then one thread per hypothesis folds the tile row in member
 // order — the same sequential FP64 chain, sample by sample, as sweep_cost (sweep.hpp:85-107).
+// Tuning switches (A/B builds only): resident CTAs per SM, the sample counter, the CTA order.
+#ifndef LFDG_SWEEP_MINB
+#define LFDG_SWEEP_MINB 4
+#endif
+#ifndef LFDG_SWEEP_COUNT
+#define LFDG_SWEEP_COUNT 1
+#endif
+#ifndef LFDG_SWEEP_ROWMAJOR
+#define LFDG_SWEEP_ROWMAJOR 1
+#endif
 template <bool kIdR, bool kCanonK>
-__global__ void __launch_bounds__(256, 4) k_sweep(const float4* __restrict__ lab, int W, int H, int nsp, int v0,
+__global__ void __launch_bounds__(256, LFDG_SWEEP_MINB) k_sweep(const float4* __restrict__ lab, int W, int H, int nsp, int v0,
                                                const Cam* __restrict__ cams, const int* __restrict__ targets,
                                                int n_targets, const int32_t* __restrict__ moff,
                                                const int32_t* __restrict__ mpix, int levels, double inv_lo,
@@ -330,11 +340,17 @@ __global__ void __launch_bounds__(256, 4) k_sweep(const float4* __restrict__ lab
     // same band of image rows in every view, so the target-image rows they gather (the epipolar
     // band of a rectified rig) stay L2-resident across source views instead of every view
     // re-streaming its targets from HBM.
-    const int row_tasks = n_views * gw;
-    const int grow = blockIdx.x / row_tasks;
-    const int rem = blockIdx.x - grow * row_tasks;
-    const int sp = grow * gw + rem % gw;
-    const int view = v0 + rem / gw;
+    int sp, view;
+    if (LFDG_SWEEP_ROWMAJOR) {
+        const int row_tasks = n_views * gw;
+        const int grow = blockIdx.x / row_tasks;
+        const int rem = blockIdx.x - grow * row_tasks;
+        sp = grow * gw + rem % gw;
+        view = v0 + rem / gw;
+    } else {
+        sp = blockIdx.x % nsp;
+        view = v0 + blockIdx.x / nsp;
+    }
     const size_t hw = (size_t)W * H;
     const int* tg = targets + (size_t)view * n_targets;
     for (int i = threadIdx.x; i < n_targets + 1; i += blockDim.x) s_cam[i] = cams[i == 0 ? view : tg[i - 1]];
@@ -395,10 +411,13 @@ __global__ void __launch_bounds__(256, 4) k_sweep(const float4* __restrict__ lab
 
     // Continue the chains of list[0, cnt) over targets [t_begin, n_targets), pruning after
     // each target (prune: keep only partial cost <= B).  Returns the surviving count.
-    unsigned long long n_samples = n_targets > 0 ? (unsigned long long)levels * n : 0;  // phase A
+    // work counter: samples of this superpixel's sweep, kept in shared memory by thread 0 (a
+    // register live across the whole kernel measurably slowed it)
+    __shared__ unsigned long long s_samples;
+    if (threadIdx.x == 0) s_samples = n_targets > 0 ? (unsigned long long)levels * n : 0;  // phase A
     auto advance = [&](int cnt, int t_begin, bool prune, double B) -> int {
         for (int ti = t_begin; ti < n_targets && cnt > 0; ++ti) {
-            n_samples += (unsigned long long)cnt * n;
+            if (LFDG_SWEEP_COUNT && threadIdx.x == 0) s_samples += (unsigned long long)cnt * n;
             const Cam& tc = s_cam[ti + 1];
             const float4* timg = lab + (size_t)tg[ti] * hw;
             for (int g0 = 0; g0 < cnt; g0 += kGroup) {
@@ -482,7 +501,7 @@ __global__ void __launch_bounds__(256, 4) k_sweep(const float4* __restrict__ lab
     }
     if (threadIdx.x == 0) {
         planes[(size_t)view * nsp + sp] = make_double4(s_d[best], 0.0, 0.0, -1.0);
-        atomicAdd(samples, n_samples);  // work counter [5]: samples of this superpixel's sweep
+        if (LFDG_SWEEP_COUNT) atomicAdd(samples, s_samples);  // work counter [5]
     }
 }
 

@@ -71,10 +71,12 @@ def main():
         pe, ce = dc.refine_work(reset=False)
         out["pix_evals_2reps"] = pe
         out["cand_evals_2reps"] = ce
-        if hasattr(dc, "work_counters"):
+        try:
             wc = dc.work_counters(reset=True)
             out["idle_pix_evals_2reps"] = wc["refine_idle_slot_evals"]
             out["sweep_samples_2reps"] = wc["sweep_samples"]
+        except Exception:  # an older library without lfdg_work_counters
+            pass
         planes = np.stack([dc.get_planes(v) for v in range(V)])
         if ref_planes is None:
             ref_planes = planes
