@@ -67,6 +67,13 @@ struct RefineArgs {
     unsigned long long* counters;
 };
 
+// many-target mode (kFlat == 3): the 8-byte gather raster (1 / depth computed per visible sample)
+// or the 16-byte one
+#ifndef LFDG_MANY_RAS8
+#define LFDG_MANY_RAS8 0
+#endif
+constexpr bool kRas8 = LFDG_MANY_RAS8;
+
 __constant__ int kDir[8][2] = {{1, 0}, {1, -1}, {0, -1}, {-1, -1}, {-1, 0}, {-1, 1}, {0, 1}, {1, 1}};
 
 // glibc lround (dbl-64 s_lround.c on x86-64) followed by static_cast<int>: |x| >= 2^63 and
@@ -215,7 +222,10 @@ struct WarpSmem {
 };
 // photo-cache slots per (lane, target): 4, or 2 in the 8-byte-raster mode (kFlat == 3: many
 // targets, where the L1 capacity the cache would take matters more than the cache hits)
-__host__ __device__ constexpr int cache_ways(int flat_mode) { return flat_mode == 3 ? 2 : 4; }
+#ifndef LFDG_MANY_WAYS
+#define LFDG_MANY_WAYS 2
+#endif
+__host__ __device__ constexpr int cache_ways(int flat_mode) { return flat_mode == 3 ? LFDG_MANY_WAYS : 4; }
 
 // lanes per candidate slot G (8, 16 or 32; 32 / G candidates share a warp): the smallest power
 // of two >= N with at least 8 lanes, except in the many-target mode (flat_mode 3) for 17..24
@@ -348,7 +358,7 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
                     // tgrid.label(px, py) and snapshot.depth[t](px, py) (refine.hpp:146-152) in one
                     // 16-byte gather: (label word, depth, 1 / (double)depth); kFlat == 3: the
                     // 8-byte raster (label word, depth), 1 / depth is computed when it is needed
-                    if (kFlat == 3) {
+                    if (kFlat == 3 && kRas8) {
                         const int2 r2 = __ldg(reinterpret_cast<const int2*>(ras) + (unsigned)(py * a.W + px));
                         rr = make_int4(r2.x, r2.y, 0, 0);
                     } else {
@@ -383,7 +393,7 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
                     const float td = __int_as_float(r.y);
                     if (td <= 0) continue;  // no target depth: not in X or Y
                     if (zt <= (double)td * (1.0 + 1e-6)) {
-                        const double rr = inv_z - (kFlat == 3 ? 1.0 / (double)td : __hiloint2double(r.w, r.z));
+                        const double rr = inv_z - (kFlat == 3 && kRas8 ? 1.0 / (double)td : __hiloint2double(r.w, r.z));
                         accumulate_vis(vis_sum, -rr * rr * a.inv_two_sigma2);
                         ++x_count;
                     } else {
@@ -630,11 +640,14 @@ __device__ __forceinline__ unsigned recheck_acceptances(const RefineArgs& a, con
 #ifndef LFDG_REFINE_MINB
 #define LFDG_REFINE_MINB 8
 #endif
+#ifndef LFDG_MANY_MINB
+#define LFDG_MANY_MINB 7
+#endif
 #ifndef LFDG_REFINE_MINB_GENERAL
 #define LFDG_REFINE_MINB_GENERAL 8
 #endif
 __host__ __device__ constexpr int refine_min_blocks(int flat_mode) {
-    return flat_mode == 3 ? 7 : flat_mode == 0 ? LFDG_REFINE_MINB_GENERAL : LFDG_REFINE_MINB;
+    return flat_mode == 3 ? LFDG_MANY_MINB : flat_mode == 0 ? LFDG_REFINE_MINB_GENERAL : LFDG_REFINE_MINB;
 }
 template <bool kIdR, bool kCanonK, int kFlat, bool kRecheck>
 __global__ void __launch_bounds__(128, refine_min_blocks(kFlat))
@@ -686,7 +699,7 @@ __global__ void __launch_bounds__(128, refine_min_blocks(kFlat))
                 TargetFlat& g = static_cast<TargetFlat*>(w.tg)[ti];
                 g.T0 = rel[9];
                 g.T1 = rel[10];
-                g.ras = kFlat == 3 ? reinterpret_cast<const int4*>(reinterpret_cast<const int2*>(a.ras) +
+                g.ras = kFlat == 3 && kRas8 ? reinterpret_cast<const int4*>(reinterpret_cast<const int2*>(a.ras) +
                                                                    (size_t)t * a.W * a.H)
                                    : a.ras + (size_t)t * a.W * a.H;
             } else {
@@ -1029,7 +1042,7 @@ void refine_iteration(Ctx& c, int l, bool recheck) {
         // the refine gather raster from the current snapshot (labels, depth)
         // many matching views on a non-linear flat rig: the 8-byte raster (kFlat == 3) halves the
         // gather working set (C4: 24 targets x a wide vertical disparity band)
-        const bool ras8 = flat_mode == 3;
+        const bool ras8 = flat_mode == 3 && kRas8;
         if (ras8)
             k_build_raster8<<<dim3(ceil_div(c.hw(), 256), c.V), 256, 0, c.stream>>>(
                 c.labels.p, c.depth.p, c.W, c.H, c.gw, reinterpret_cast<int2*>(c.ras.p));
@@ -1061,7 +1074,7 @@ void refine_iteration(Ctx& c, int l, bool recheck) {
             if (flat) {
                 if (a.row_inv)
                     launch(k_refine<true, true, 2, R>);
-                else if (ras8)
+                else if (flat_mode == 3)
                     launch(k_refine<true, true, 3, R>);
                 else
                     launch(k_refine<true, true, 1, R>);
