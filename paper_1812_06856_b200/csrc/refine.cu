@@ -301,13 +301,13 @@ __device__ __forceinline__ PixGeo pixel_geo(const RefineArgs& a, const double2* 
 // per pixel (one lane per pixel) and broadcast through shared memory.  The label cache is backed
 // by a small lane-private cache of photo weights, which are pure functions of (task colour,
 // target, label) and so stay valid for the whole task.  V + O are summed in target order.
-template <bool kIdR, bool kCanonK, int kFlat>
+template <bool kIdR, bool kCanonK, int kFlat, int kG>
 __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const WarpSmem& w, int v, int sp, double4 p,
                                                    int m0, int n) {
     const int lane = threadIdx.x & 31;
     const int N = a.N;
     if (N == 0) return 1.0;
-    const int G = lanes_per_candidate(N, kFlat);
+    const int G = kG ? kG : lanes_per_candidate(N, kFlat);  // lanes per candidate slot
     const int cs = lane / G;  // candidate slot
     const int tl = lane % G;  // target lane
     const size_t hw = (size_t)a.W * a.H;
@@ -476,7 +476,7 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
 // accepted either) — so the accepted planes and the count are the reference's.
 // init: cand[0] is the current plane and its energy initialises e_cur (refine.hpp:277).
 // current: index in cand of the running plane.
-template <bool kIdR, bool kCanonK, int kFlat, bool kRecheck>
+template <bool kIdR, bool kCanonK, int kFlat, bool kRecheck, int kG>
 __device__ __forceinline__ void greedy(const RefineArgs& a, const WarpSmem& w, int base, int n, int v, int sp, int m0,
                                        int n_members, bool init, double& e_cur, int& current, unsigned& accepted,
                                        unsigned long long& pix_evals, unsigned& cand_evals,
@@ -484,7 +484,7 @@ __device__ __forceinline__ void greedy(const RefineArgs& a, const WarpSmem& w, i
     // (accepted also indexes w.acc: the recheck list of this task's acceptances)
     const int lane = threadIdx.x & 31;
     const bool prune = a.use_s && a.use_c;
-    const int G = lanes_per_candidate(a.N, kFlat);
+    const int G = kG ? kG : lanes_per_candidate(a.N, kFlat);
     const int slots = init ? 1 : 32 / G;
     int next = base;
     n += base;
@@ -520,7 +520,7 @@ __device__ __forceinline__ void greedy(const RefineArgs& a, const WarpSmem& w, i
         idle_evals += (unsigned long long)(slots - cnt) * a.N * n_members;
         double ec = 0;
         if (a.use_c) {
-            ec = consistency_pair<kIdR, kCanonK, kFlat>(a, w, v, sp, w.cand[mine], m0, n_members);
+            ec = consistency_pair<kIdR, kCanonK, kFlat, kG>(a, w, v, sp, w.cand[mine], m0, n_members);
             pix_evals += (unsigned long long)a.N * n_members * cnt;
         }
         cand_evals += cnt;
@@ -589,11 +589,11 @@ __device__ void smoothness_all(const RefineArgs& a, const WarpSmem& w, int base,
 // snapshot — smoothness_term and consistency_term recomputed, multiplied in energy()'s order
 // (refine.hpp:201-207) — and an acceptance whose candidate does not strictly beat its
 // predecessor counts as a violation.  Only in stats mode (the reference pays the same price).
-template <bool kIdR, bool kCanonK, int kFlat>
+template <bool kIdR, bool kCanonK, int kFlat, int kG>
 __device__ __forceinline__ unsigned recheck_acceptances(const RefineArgs& a, const WarpSmem& w, int v, int sp, int m0, int n_members,
                                         unsigned n_acc) {
     const int lane = threadIdx.x & 31;
-    const int G = lanes_per_candidate(a.N, kFlat);
+    const int G = kG ? kG : lanes_per_candidate(a.N, kFlat);
     const int slots = 32 / G;
     unsigned violations = 0;
     for (unsigned k = 0; k < n_acc; ++k) {
@@ -612,12 +612,12 @@ __device__ __forceinline__ unsigned recheck_acceptances(const RefineArgs& a, con
         if (a.use_c) {
             if (slots >= 2) {
                 const int mine = lane / G == 0 ? pr.x : pr.y;
-                const double r = consistency_pair<kIdR, kCanonK, kFlat>(a, w, v, sp, w.cand[mine], m0, n_members);
+                const double r = consistency_pair<kIdR, kCanonK, kFlat, kG>(a, w, v, sp, w.cand[mine], m0, n_members);
                 ec[0] = __shfl_sync(LFDG_FULL_MASK, r, 0);
                 ec[1] = __shfl_sync(LFDG_FULL_MASK, r, G);
             } else {
-                ec[0] = consistency_pair<kIdR, kCanonK, kFlat>(a, w, v, sp, w.cand[pr.x], m0, n_members);
-                ec[1] = consistency_pair<kIdR, kCanonK, kFlat>(a, w, v, sp, w.cand[pr.y], m0, n_members);
+                ec[0] = consistency_pair<kIdR, kCanonK, kFlat, kG>(a, w, v, sp, w.cand[pr.x], m0, n_members);
+                ec[1] = consistency_pair<kIdR, kCanonK, kFlat, kG>(a, w, v, sp, w.cand[pr.y], m0, n_members);
             }
         }
         double en[2];
@@ -649,7 +649,7 @@ __device__ __forceinline__ unsigned recheck_acceptances(const RefineArgs& a, con
 __host__ __device__ constexpr int refine_min_blocks(int flat_mode) {
     return flat_mode == 3 ? LFDG_MANY_MINB : flat_mode == 0 ? LFDG_REFINE_MINB_GENERAL : LFDG_REFINE_MINB;
 }
-template <bool kIdR, bool kCanonK, int kFlat, bool kRecheck>
+template <bool kIdR, bool kCanonK, int kFlat, bool kRecheck, int kG>
 __global__ void __launch_bounds__(128, refine_min_blocks(kFlat))
     k_refine(RefineArgs a, int n_tasks, int* task_counter, int cap, double4* g_cand, double* g_es, int2* g_acc) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -724,7 +724,7 @@ __global__ void __launch_bounds__(128, refine_min_blocks(kFlat))
         __syncwarp();
         if (a.use_s) smoothness_all(a, w, 0, 1, v, sp);
         mark_repeats(a, w, 0, 1);
-        greedy<kIdR, kCanonK, kFlat, kRecheck>(a, w, 0, 1, v, sp, m0, n_members, true, e_cur, current, accepted, pix_evals,
+        greedy<kIdR, kCanonK, kFlat, kRecheck, kG>(a, w, 0, 1, v, sp, m0, n_members, true, e_cur, current, accepted, pix_evals,
                                      cand_evals, idle_evals);
 
         // ---- phase A: grid_neighbors(Kernel) order (superpixel.hpp:318-343), re-anchored
@@ -771,7 +771,7 @@ __global__ void __launch_bounds__(128, refine_min_blocks(kFlat))
         __syncwarp();
         if (a.use_s) smoothness_all(a, w, 1, n_cand, v, sp);
         mark_repeats(a, w, 1, 1 + n_cand);
-        greedy<kIdR, kCanonK, kFlat, kRecheck>(a, w, 1, n_cand, v, sp, m0, n_members, false, e_cur, current, accepted, pix_evals,
+        greedy<kIdR, kCanonK, kFlat, kRecheck, kG>(a, w, 1, n_cand, v, sp, m0, n_members, false, e_cur, current, accepted, pix_evals,
                                      cand_evals, idle_evals);
 
         // ---- phase B: normal_candidates (refine.hpp:213-242) at the phase-A depth
@@ -817,14 +817,14 @@ __global__ void __launch_bounds__(128, refine_min_blocks(kFlat))
             const int nn = __popc(m);
             if (a.use_s) smoothness_all(a, w, 1 + n_cand, nn, v, sp);
             mark_repeats(a, w, 1 + n_cand, 1 + n_cand + nn);
-            greedy<kIdR, kCanonK, kFlat, kRecheck>(a, w, 1 + n_cand, nn, v, sp, m0, n_members, false, e_cur, current, accepted,
+            greedy<kIdR, kCanonK, kFlat, kRecheck, kG>(a, w, 1 + n_cand, nn, v, sp, m0, n_members, false, e_cur, current, accepted,
                                          pix_evals, cand_evals, idle_evals);
         }
         if (lane == 0) a.out[vs + sp] = w.cand[current];
         accepted_total += accepted;
         if (kRecheck && accepted) {
             __syncwarp();
-            violations_total += recheck_acceptances<kIdR, kCanonK, kFlat>(a, w, v, sp, m0, n_members, accepted);
+            violations_total += recheck_acceptances<kIdR, kCanonK, kFlat, kG>(a, w, v, sp, m0, n_members, accepted);
         }
         __syncwarp();
     }
@@ -1069,23 +1069,26 @@ void refine_iteration(Ctx& c, int l, bool recheck) {
         // z = 0 (then every rel_trans.z = 0): the rectified / grid rigs of the fixtures.
         // kRecheck (stats mode): a separate instantiation carries the re-check, so the hot
         // variant's register allocation is untouched by it
-        auto pick = [&](auto rc) {
+        // kG: lanes per candidate slot as a compile-time constant for the hot (non-stats) variants
+        // (the slot / target-lane arithmetic then folds to shifts and masks)
+        auto pick = [&](auto rc, auto gc) {
             constexpr bool R = decltype(rc)::value;
+            constexpr int KG = decltype(gc)::value;
             if (flat) {
                 if (a.row_inv)
-                    launch(k_refine<true, true, 2, R>);
+                    launch(k_refine<true, true, 2, R, KG>);
                 else if (flat_mode == 3)
-                    launch(k_refine<true, true, 3, R>);
+                    launch(k_refine<true, true, 3, R, KG>);
                 else
-                    launch(k_refine<true, true, 1, R>);
+                    launch(k_refine<true, true, 1, R, KG>);
             } else if (c.identity_rot && c.canonical_k) {
-                launch(k_refine<true, true, 0, R>);
+                launch(k_refine<true, true, 0, R, KG>);
             } else if (c.identity_rot) {
-                launch(k_refine<true, false, 0, R>);
+                launch(k_refine<true, false, 0, R, KG>);
             } else if (c.canonical_k) {
-                launch(k_refine<false, true, 0, R>);
+                launch(k_refine<false, true, 0, R, KG>);
             } else {
-                launch(k_refine<false, false, 0, R>);
+                launch(k_refine<false, false, 0, R, KG>);
             }
         };
         if (flat) {
@@ -1094,10 +1097,15 @@ void refine_iteration(Ctx& c, int l, bool recheck) {
             a.uK11 = c.cams[0].K[4];
             a.uK12 = c.cams[0].K[5];
         }
+        const int G = lanes_per_candidate(a.N, flat_mode);
         if (recheck)
-            pick(std::true_type{});
+            pick(std::true_type{}, std::integral_constant<int, 0>{});
+        else if (G == 8)
+            pick(std::false_type{}, std::integral_constant<int, 8>{});
+        else if (G == 16)
+            pick(std::false_type{}, std::integral_constant<int, 16>{});
         else
-            pick(std::false_type{});
+            pick(std::false_type{}, std::integral_constant<int, 32>{});
         LFDG_LAUNCHED(&c);
         LFDG_CUDA_CHECK(cudaMemcpyAsync(c.planes.p + (size_t)rv0 * c.nsp, c.planes_next.p + (size_t)rv0 * c.nsp,
                                         (size_t)rn * c.nsp * sizeof(double4), cudaMemcpyDeviceToDevice, c.stream));
