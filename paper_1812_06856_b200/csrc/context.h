@@ -171,6 +171,7 @@ struct Ctx {
     DevBuf<double4> planes, planes_next;
     DevBuf<float> depth;
     DevBuf<int> sweep_targets;  // [V][N] matching views of the last sweep
+    DevBuf<unsigned char> sweep_scratch;  // per-resident-CTA hypothesis slots for L beyond shared memory
     DevBuf<float> fused;        // [V][H*W] stability-fused depth (fusion.hpp:94)
     DevBuf<int4> ras;    // [V][H*W] refine gather raster: (label word, depth, 1/depth), see refine.cu
 

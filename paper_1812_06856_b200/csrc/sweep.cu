@@ -312,13 +312,14 @@ __device__ int block_compact(int levels, int* list, int* s_cnt, Pred keep) {
 #ifndef LFDG_SWEEP_ROWMAJOR
 #define LFDG_SWEEP_ROWMAJOR 1
 #endif
-template <bool kIdR, bool kCanonK>
+template <bool kIdR, bool kCanonK, bool kScratch>
 __global__ void __launch_bounds__(256, LFDG_SWEEP_MINB) k_sweep(const float4* __restrict__ lab, int W, int H, int nsp, int v0,
                                                const Cam* __restrict__ cams, const int* __restrict__ targets,
                                                int n_targets, const int32_t* __restrict__ moff,
                                                const int32_t* __restrict__ mpix, int levels, double inv_lo,
                                                double inv_hi, double step, float T, uint64_t seed, int gw,
-                                               int n_views, double4* planes, unsigned long long* samples) {
+                                               int n_views, double4* planes, unsigned long long* samples,
+                                               unsigned char* __restrict__ gscr, size_t slot_bytes, int cta0) {
     extern __shared__ __align__(16) unsigned char smem[];
     // [staging / tile union][cams][s_d][s_P][list]
     constexpr size_t kUnion = kSweepCap * (sizeof(double2) + sizeof(float4)) > kGroup * kTilePitch * sizeof(float)
@@ -328,7 +329,17 @@ __global__ void __launch_bounds__(256, LFDG_SWEEP_MINB) k_sweep(const float4* __
     float4* s_ref = reinterpret_cast<float4*>(smem + kSweepCap * sizeof(double2));
     float* s_tile = reinterpret_cast<float*>(smem);
     Cam* s_cam = reinterpret_cast<Cam*>(smem + kUnion);
-    double* s_d = reinterpret_cast<double*>(smem + kUnion + (size_t)(n_targets + 1) * sizeof(Cam));
+    // the per-hypothesis arrays: in shared memory, or (levels beyond the shared-memory budget) in
+    // this CTA's slot of a global scratch buffer, the launch then covering CTAs [cta0, cta0 + grid)
+    double* s_d;
+    int* s_tmp;  // prune-list staging: the (then free) sample tile, or the scratch slot
+    if (kScratch) {
+        s_d = reinterpret_cast<double*>(gscr + (size_t)blockIdx.x * slot_bytes);
+        s_tmp = reinterpret_cast<int*>(s_d + 2 * (size_t)levels) + levels;
+    } else {
+        s_d = reinterpret_cast<double*>(smem + kUnion + (size_t)(n_targets + 1) * sizeof(Cam));
+        s_tmp = reinterpret_cast<int*>(smem);
+    }
     double* s_P = s_d + levels;
     int* s_list = reinterpret_cast<int*>(s_P + levels);
     __shared__ double red_c[32], red_d[32];
@@ -343,13 +354,15 @@ __global__ void __launch_bounds__(256, LFDG_SWEEP_MINB) k_sweep(const float4* __
     int sp, view;
     if (LFDG_SWEEP_ROWMAJOR) {
         const int row_tasks = n_views * gw;
-        const int grow = blockIdx.x / row_tasks;
-        const int rem = blockIdx.x - grow * row_tasks;
+        const int cta = (kScratch ? cta0 : 0) + (int)blockIdx.x;
+        const int grow = cta / row_tasks;
+        const int rem = cta - grow * row_tasks;
         sp = grow * gw + rem % gw;
         view = v0 + rem / gw;
     } else {
-        sp = blockIdx.x % nsp;
-        view = v0 + blockIdx.x / nsp;
+        const int cta = (kScratch ? cta0 : 0) + (int)blockIdx.x;
+        sp = cta % nsp;
+        view = v0 + cta / nsp;
     }
     const size_t hw = (size_t)W * H;
     const int* tg = targets + (size_t)view * n_targets;
@@ -471,7 +484,7 @@ __global__ void __launch_bounds__(256, LFDG_SWEEP_MINB) k_sweep(const float4* __
             }
             if (prune) {
                 // keep list members whose partial cost is still <= B (ordered, in place)
-                int* tmp = reinterpret_cast<int*>(s_tile);  // tile is free here
+                int* tmp = s_tmp;
                 for (int q = threadIdx.x; q < cnt; q += blockDim.x) tmp[q] = s_list[q];
                 __syncthreads();
                 cnt = block_compact(cnt, s_list, red_k, [&](int q) { return s_P[tmp[q]] <= B; });
@@ -557,9 +570,6 @@ std::vector<int> matching_views(const Ctx& c, int view, int max_neighbors) {
 
 void sweep_views(Ctx& c, int v0, int n, const lfdg_sweep_params& p, uint64_t seed) {
     if (p.levels < 2) throw Error(LFDG_INVALID_PARAMS, "sweep levels must be >= 2");
-    // the hypotheses of one superpixel live in shared memory (and the prune list in the tile,
-    // kGroup * kTilePitch ints): up to 8192 levels
-    if (p.levels > 8192) throw Error(LFDG_INVALID_PARAMS, "sweep levels > 8192 are not supported");
     if (!(p.tssd_threshold > 0)) throw Error(LFDG_INVALID_PARAMS, "tssd threshold must be > 0");
     if (!(0 < c.d_min && c.d_min < c.d_max)) throw Error(LFDG_INVARIANT, "depth range requires 0 < d_min < d_max");
     if (v0 < 0 || n < 0 || v0 + n > c.V) throw Error(LFDG_STATE, "view range out of bounds");
@@ -579,24 +589,49 @@ void sweep_views(Ctx& c, int v0, int n, const lfdg_sweep_params& p, uint64_t see
     const double inv_hi = 1.0 / c.d_min;
     const double step = (inv_hi - inv_lo) / (p.levels - 1);
     const int threads = 256;
-    const size_t smem = std::max(kSweepCap * (sizeof(double2) + sizeof(float4)), kGroup * kTilePitch * sizeof(float)) +
-                        (size_t)(nt + 1) * sizeof(Cam) + (size_t)p.levels * (2 * sizeof(double) + sizeof(int));
+    // The hypotheses of a superpixel (depth, partial cost, list: 20 B each) live in shared memory
+    // while they fit beside the tile — with the prune list staged in the tile (kGroup * kTilePitch
+    // ints) — and otherwise in global scratch slots, one per resident CTA, the grid then launched
+    // in waves of that many CTAs (the reference accepts any L >= 2).
+    const size_t fixed = std::max(kSweepCap * (sizeof(double2) + sizeof(float4)), kGroup * kTilePitch * sizeof(float)) +
+                         (size_t)(nt + 1) * sizeof(Cam);
+    const size_t in_smem = fixed + (size_t)p.levels * (2 * sizeof(double) + sizeof(int));
+    const bool scratch = p.levels > kGroup * kTilePitch || in_smem > (size_t)(227 * 1024);
+    const size_t smem = scratch ? fixed : in_smem;
+    if (smem > (size_t)(227 * 1024))
+        throw Error(LFDG_INVALID_PARAMS, "too many matching views for the sweep's shared-memory camera table");
     const unsigned grid = (unsigned)c.nsp * (unsigned)n;
-    auto launch = [&](auto kernel) {
-        LFDG_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kernel<<<grid, threads, smem, c.stream>>>(c.lab.p, c.W, c.H, c.nsp, v0, c.d_cams.p, d_tg.p, nt, c.moff.p,
-                                                  c.mpix.p, p.levels, inv_lo, inv_hi, step, p.tssd_threshold, seed, c.gw,
-                                                  n, c.planes.p, c.counters.p + 5);
+    const size_t slot_bytes = ((size_t)p.levels * (2 * sizeof(double) + 2 * sizeof(int)) + 255) & ~(size_t)255;
+    auto launch = [&](auto kernel, auto kernel_scratch) {
+        if (!scratch) {
+            LFDG_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            kernel<<<grid, threads, smem, c.stream>>>(c.lab.p, c.W, c.H, c.nsp, v0, c.d_cams.p, d_tg.p, nt, c.moff.p,
+                                                      c.mpix.p, p.levels, inv_lo, inv_hi, step, p.tssd_threshold, seed,
+                                                      c.gw, n, c.planes.p, c.counters.p + 5, nullptr, 0, 0);
+            LFDG_LAUNCHED(&c);
+            return;
+        }
+        LFDG_CUDA_CHECK(cudaFuncSetAttribute(kernel_scratch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0;
+        LFDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel_scratch, threads, smem));
+        const unsigned wave = std::min<unsigned>(grid, (unsigned)std::max(per_sm, 1) * (unsigned)c.sm_count);
+        c.sweep_scratch.alloc(wave * slot_bytes);
+        for (unsigned off = 0; off < grid; off += wave) {
+            kernel_scratch<<<std::min(wave, grid - off), threads, smem, c.stream>>>(
+                c.lab.p, c.W, c.H, c.nsp, v0, c.d_cams.p, d_tg.p, nt, c.moff.p, c.mpix.p, p.levels, inv_lo, inv_hi,
+                step, p.tssd_threshold, seed, c.gw, n, c.planes.p, c.counters.p + 5, c.sweep_scratch.p, slot_bytes,
+                (int)off);
+            LFDG_LAUNCHED(&c);
+        }
     };
     if (c.identity_rot && c.canonical_k)
-        launch(k_sweep<true, true>);
+        launch(k_sweep<true, true, false>, k_sweep<true, true, true>);
     else if (c.identity_rot)
-        launch(k_sweep<true, false>);
+        launch(k_sweep<true, false, false>, k_sweep<true, false, true>);
     else if (c.canonical_k)
-        launch(k_sweep<false, true>);
+        launch(k_sweep<false, true, false>, k_sweep<false, true, true>);
     else
-        launch(k_sweep<false, false>);
-    LFDG_LAUNCHED(&c);
+        launch(k_sweep<false, false, false>, k_sweep<false, false, true>);
     for (int b = 0; b < n; ++b) c.planes_ready[v0 + b] = 1;
 }
 

@@ -153,7 +153,7 @@ def test_many_matching_views(ref, grid):
 def test_hundreds_of_matching_views(ref):
     """Inputs the reference accepts at any size: 320 views (N = 319 matching views, off-plane
     camera centres so the general refine kernel runs with its per-target tables; shared memory
-    then holds two warps per CTA instead of four) and 5000 sweep levels.  Sampled sweep winners and
+    then holds two warps per CTA instead of four) and 5000 / 20000 sweep levels.  Sampled sweep winners and
     refine tasks are compared with the reference."""
     from paper_1812_06856_b200 import api
 
@@ -198,3 +198,9 @@ def test_hundreds_of_matching_views(ref):
         rs2.slic(v, 12, 0.1, 10)
     got = dc2.sweep(0, api.SweepParams(5000, 0.05, 0), 3)
     assert np.array_equal(got, rs2.sweep(0, 5000, 0.05, 0, 3))
+    # 20000 levels: beyond shared memory, the hypotheses live in global scratch slots and the
+    # superpixels are swept in waves of resident CTAs
+    got = dc2.sweep(1, api.SweepParams(20000, 0.05, 0), 5)
+    assert np.array_equal(got, rs2.sweep(1, 20000, 0.05, 0, 5))
+    dc2.sweep_views(0, 3, api.SweepParams(20000, 0.05, 0), 5)
+    assert np.array_equal(dc2.get_planes(1), got)
