@@ -1017,6 +1017,9 @@ void refine_iteration(Ctx& c, int l, bool recheck) {
     for (const lfdg_camera& k : c.cams)
         flat = flat && k.t[2] == 0.0 && k.K[0] == c.cams[0].K[0] && k.K[2] == c.cams[0].K[2] &&
                k.K[4] == c.cams[0].K[4] && k.K[5] == c.cams[0].K[5];
+    // the flat-rig kernels' fast lround needs image sides <= 2^20; wider images take the general
+    // kernels (exact for any rig)
+    if (c.W > (1 << 20) || c.H > (1 << 20)) flat = false;
     if (flat) {
         a.row_inv = 1;
         for (int vv = 0; vv < c.V; ++vv)
@@ -1030,8 +1033,6 @@ void refine_iteration(Ctx& c, int l, bool recheck) {
     // kFlat mode: 2 linear rig (row-invariant targets), 3 many targets with the 8-byte raster,
     // 1 other flat rigs, 0 general
     const int flat_mode = !flat ? 0 : a.row_inv ? 2 : a.N > 16 ? 3 : 1;
-    if (flat_mode && (c.W > (1 << 20) || c.H > (1 << 20)))
-        throw Error(LFDG_INVALID_PARAMS, "refinement supports images up to 2^20 pixels wide / high");
     // four warps per CTA; fewer when the per-warp tables (which grow with the number of matching
     // views) would not fit the 227 KB of shared memory of a CTA — one warp holds ~1000 targets
     const size_t wbytes = warp_smem_bytes(a.N, flat_mode);

@@ -115,19 +115,25 @@ def test_rig_fusion(rig):
         assert np.array_equal(got.view(np.uint32), want[v].view(np.uint32)), f"{kind}: fused view {v}"
 
 
-@pytest.mark.parametrize("grid", [(4, 5), (0, 0)])
+@pytest.mark.parametrize("grid", [(4, 5), (0, 0), "jittered"])
 def test_many_matching_views(ref, grid):
     """All-others matching with many targets, every stage bit-exact against the reference:
     a 4x5 grid rig, N = 19 (the many-target mode: groups of 8 lanes over three target rounds, the
-    last one partial), and 70 views on a line, N = 69 (groups of 32 lanes over three rounds, the
-    wide photo cache)."""
+    last one partial), the same grid with every camera centre jittered in x and y (every target
+    translation distinct), and 70 views on a line, N = 69 (groups of 32
+    lanes over three rounds, the wide photo cache).  Iteration 1 runs with RefineStats (the
+    re-check instantiation), iteration 2 without (the hot instantiation)."""
     from paper_1812_06856_b200 import api
 
-    sc = ref.render_scene("cluttered", 70, 64, 48, 64.0, 0.01, grid=grid)
+    sc = ref.render_scene("cluttered", 70, 64, 48, 64.0, 0.01, grid=(4, 5) if grid == "jittered" else grid)
+    cams = sc["cams"].copy()
+    if grid == "jittered":
+        jit = np.random.default_rng(11).uniform(-0.002, 0.002, (cams.shape[0], 2))
+        cams[:, 18:20] += jit  # t.x, t.y; t.z stays 0 (kFlat)
     nv = sc["lab"].shape[0]
-    rs = ref.Session(sc["lab"], sc["cams"], sc["range"])
+    rs = ref.Session(sc["lab"], cams, sc["range"])
     dc = api.DeviceContext(0)
-    dc.set_views(sc["lab"], sc["cams"], sc["range"])
+    dc.set_views(sc["lab"], cams, sc["range"])
     for v in range(nv):
         rs.slic(v, 8, 0.1, 10)
         dc.slic(v, api.SlicParams(8, 0.1, 10))
@@ -148,6 +154,12 @@ def test_many_matching_views(ref, grid):
     for v in range(nv):
         assert np.array_equal(dc.get_planes(v), rs.planes(v)), f"refine view {v}"
     assert acc_g == acc_r
+    rs.rasterize()
+    dc.rasterize()
+    rs.refine_iteration(2, with_stats=False)
+    dc.refine_iteration(2, with_stats=False)
+    for v in range(nv):
+        assert np.array_equal(dc.get_planes(v), rs.planes(v)), f"refine l=2 view {v}"
 
 
 def test_hundreds_of_matching_views(ref):
