@@ -107,6 +107,9 @@ int lfdg_set_views(lfdg_ctx* p, int n_views, int width, int height, const float*
         auto* c = C(p);
         activate(c);
         if (n_views < 1 || width < 1 || height < 1) throw lfdg::Error(LFDG_INVALID_PARAMS, "invalid view set shape");
+        // pixel indices are 32-bit (member CSR, gather rasters, texel offsets)
+        if ((size_t)width * height >= ((size_t)1 << 31))
+            throw lfdg::Error(LFDG_INVALID_PARAMS, "views of 2^31 pixels or more are not supported");
         if (!images || !cameras) throw lfdg::Error(LFDG_STATE, "null images / cameras");
         if (!(0 < d_min && d_min < d_max)) throw lfdg::Error(LFDG_INVARIANT, "depth range requires 0 < d_min < d_max");
         c->V = n_views;

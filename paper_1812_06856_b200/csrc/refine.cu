@@ -257,6 +257,28 @@ __device__ __noinline__ double photo_miss(const int* target, const float4* ref, 
     return libm::exp_nonpos(-(double)color_dist2(rc.x, rc.y, rc.z, c.x, c.y, c.z) * inv_two_alpha2);
 }
 
+// The photo-cache row of a lane addressed by its 32-bit shared-window offset, made opaque to the
+// compiler (LFDG_PC_S32 = 2) so that it stays in one register: the generic row pointer was
+// rematerialised from the lane id on every cache probe (8 instructions; refine -3.6 / -1.5 /
+// -3.2 % at C3 / C4 / C5).  0: plain pointer (A/B builds only).
+#ifndef LFDG_PC_S32
+#define LFDG_PC_S32 2
+#endif
+__device__ __forceinline__ double2 pc_load(const double2* base, unsigned base_s, int way) {
+    if (LFDG_PC_S32) {
+        double2 v;
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(base_s + 16u * way));
+        return v;
+    }
+    return base[way];
+}
+__device__ __forceinline__ void pc_store(double2* base, unsigned base_s, int way, double2 v) {
+    if (LFDG_PC_S32)
+        asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(base_s + 16u * way), "d"(v.x), "d"(v.y) : "memory");
+    else
+        base[way] = v;
+}
+
 // Per-pixel geometry of member pixel i for plane p (refine.hpp:131-137).
 template <int kFlat>
 __device__ __forceinline__ PixGeo pixel_geo(const RefineArgs& a, const double2* mr, int i, int n, double4 p,
@@ -323,6 +345,8 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
         const bool act = t < N;
         double2* const pcl =  // this lane's cache row
             w.pc + (kFlat == 3 ? cs * ((N + G - 1) / G * G) + t : lane + t0) * (cache_ways(kFlat) + 1);
+        unsigned pcl_s = (unsigned)__cvta_generic_to_shared(pcl);
+        if (LFDG_PC_S32 > 1) asm volatile("mov.u32 %0, %0;" : "+r"(pcl_s));  // opaque: kept, not recomputed
         double T0 = 0, T1 = 0;
         const int4* ras = nullptr;
         if (kFlat && act) {
@@ -378,14 +402,13 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
                     const double zt = qc->sv2, inv_z = qc->f_inv;
                     if (r.x != cached_word) {  // refine.hpp:147-150
                         const int way = (((unsigned)r.x >> 28) + 2 * ((unsigned)r.x >> 30)) & (cache_ways(kFlat) - 1);
-                        double2* e = pcl + way;
-                        const double2 c = *e;
+                        const double2 c = pc_load(pcl, pcl_s, way);
                         if (__double2loint(c.y) == r.x) {
                             cached_w = c.x;
                         } else {
                             cached_w = photo_miss(a.targets + (size_t)v * N + t, a.color + (size_t)v * a.nsp + sp,
                                                   a.color, a.nsp, r.x & 0x0FFFFFFF, a.inv_two_alpha2);
-                            *e = make_double2(cached_w, __hiloint2double(-1, r.x));
+                            pc_store(pcl, pcl_s, way, make_double2(cached_w, __hiloint2double(-1, r.x)));
                         }
                         cached_word = r.x;
                     }
@@ -429,14 +452,13 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
                     const int4 r = __ldg(g.ras + (unsigned)(py * a.W + px));
                     if (r.x != cached_word) {  // refine.hpp:147-150
                         const int way = (((unsigned)r.x >> 28) + 2 * ((unsigned)r.x >> 30)) & (cache_ways(kFlat) - 1);
-                        double2* e = pcl + way;
-                        const double2 c = *e;
+                        const double2 c = pc_load(pcl, pcl_s, way);
                         if (__double2loint(c.y) == r.x) {
                             cached_w = c.x;
                         } else {
                             cached_w = photo_miss(a.targets + (size_t)v * N + t, a.color + (size_t)v * a.nsp + sp,
                                                   a.color, a.nsp, r.x & 0x0FFFFFFF, a.inv_two_alpha2);
-                            *e = make_double2(cached_w, __hiloint2double(-1, r.x));
+                            pc_store(pcl, pcl_s, way, make_double2(cached_w, __hiloint2double(-1, r.x)));
                         }
                         cached_word = r.x;
                     }
