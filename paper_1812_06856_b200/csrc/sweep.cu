@@ -26,6 +26,17 @@
 namespace lfdg {
 namespace {
 
+// Sample addressing (A/B switches): 32-bit texel indices, and the target image's base pointer
+// made opaque to the compiler so that it stays in registers — it was rematerialised from
+// (target id, W*H) with a 64-bit multiply chain on every sample (sweep 126 -> 116 ms at C3,
+// 236 -> 217 ms at C5, 250 -> 243 ms on the converging rig).
+#ifndef LFDG_SWEEP_ADDR32
+#define LFDG_SWEEP_ADDR32 1
+#endif
+#ifndef LFDG_SWEEP_OPAQUE
+#define LFDG_SWEEP_OPAQUE 1
+#endif
+
 constexpr int kSweepCap = 1024;  // member pixels staged per chunk
 
 // Packed f32x2 arithmetic (two colour channels per instruction).  Products go through
@@ -90,9 +101,18 @@ __device__ __forceinline__ float tssd_row(const float4* __restrict__ timg, int W
     const int y0 = row.y0;
     const float fx = (float)(u - x0);
     const float fy = row.fy;
+#if LFDG_SWEEP_ADDR32
+    // 32-bit texel indices (a view has < 2^31 pixels, checked by set_views): two address
+    // computations instead of a 64-bit multiply-add chain per sample
+    const unsigned i0 = (unsigned)(y0 * W + x0);
+    const float4* r0 = timg + i0;
+    const float4* r1 = timg + (i0 + (unsigned)W);
+#else
     const float4* r0 = timg + ((size_t)y0 * W + x0);
+    const float4* r1 = r0 + W;
+#endif
     const float4 p00 = __ldg(r0), p10 = __ldg(r0 + 1);
-    const float4 p01 = __ldg(r0 + W), p11 = __ldg(r0 + W + 1);
+    const float4 p01 = __ldg(r1), p11 = __ldg(r1 + 1);
     const unsigned long long FX = f2pack(fx, fx), FY = f2pack(fy, fy);
     const unsigned long long a00 = f2pack(p00.x, p00.y), a10 = f2pack(p10.x, p10.y);
     const unsigned long long a01 = f2pack(p01.x, p01.y), a11 = f2pack(p11.x, p11.y);
@@ -390,6 +410,7 @@ __global__ void __launch_bounds__(256, LFDG_SWEEP_MINB) k_sweep(const float4* __
         if (n_targets > 0) {
             const Cam& tc = s_cam[1];
             const float4* timg = lab + (size_t)tg[0] * hw;
+            if (LFDG_SWEEP_OPAQUE) asm volatile("mov.b64 %0, %0;" : "+l"(timg));  // kept, not recomputed per sample
             for (int c0 = 0; c0 < n; c0 += kSweepCap) {
                 if (n > kSweepCap || (c0 == 0 && r == 0)) {
                     __syncthreads();
@@ -433,6 +454,7 @@ __global__ void __launch_bounds__(256, LFDG_SWEEP_MINB) k_sweep(const float4* __
             if (LFDG_SWEEP_COUNT && threadIdx.x == 0) s_samples += (unsigned long long)cnt * n;
             const Cam& tc = s_cam[ti + 1];
             const float4* timg = lab + (size_t)tg[ti] * hw;
+            if (LFDG_SWEEP_OPAQUE) asm volatile("mov.b64 %0, %0;" : "+l"(timg));  // kept, not recomputed per sample
             for (int g0 = 0; g0 < cnt; g0 += kGroup) {
                 const int gn = min(kGroup, cnt - g0);
                 if (threadIdx.x < gn) {
