@@ -261,6 +261,10 @@ __device__ __noinline__ double photo_miss(const int* target, const float4* ref, 
 // compiler (LFDG_PC_S32 = 2) so that it stays in one register: the generic row pointer was
 // rematerialised from the lane id on every cache probe (8 instructions; refine -3.6 / -1.5 /
 // -3.2 % at C3 / C4 / C5).  0: plain pointer (A/B builds only).
+// LFDG_SKIP_OK: the kFlat 2 gather skips the per-pixel ok test (refine -3.5 / -3.3 % at C3 / C5).
+#ifndef LFDG_SKIP_OK
+#define LFDG_SKIP_OK 1
+#endif
 #ifndef LFDG_PC_S32
 #define LFDG_PC_S32 2
 #endif
@@ -368,7 +372,9 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
                 // Software-pipelined by one pixel: the raster record of pixel jj + 1 is requested
                 // before pixel jj is consumed, so the gather's latency overlaps the exp.
                 auto issue = [&](const PixGeo* qq, int4& rr) -> bool {
-                    if (!qq->ok) return false;
+                    // kFlat == 2: an invisible pixel has f_py = -1, so the bounds test below rejects
+                    // it without the ok test (its column is computed from zeros and discarded)
+                    if (!(kFlat == 2 && LFDG_SKIP_OK) && !qq->ok) return false;
                     int px, py;
                     const double hx = a.uK00 * (qq->sv0 + T0) + qq->f_kz0;
                     if (!fast_lround_img(hx * qq->f_inv, px)) px = lround_div(hx, qq->sv2);
