@@ -89,7 +89,8 @@ __device__ __forceinline__ int lround_int(double x) {
 }
 
 // lround(h / z) the slow way (division, then lround), out of line: fast_lround's rare fallback.
-__device__ __noinline__ int lround_div(double h, double z) { return lround_int(h / z); }
+// z = NaN marks an invisible pixel of the flat-rig modes 1 / 3 (pixel_geo): -1, outside any image.
+__device__ __noinline__ int lround_div(double h, double z) { return z == z ? lround_int(h / z) : -1; }
 
 // exp of the visibility term (refine.hpp:158): glibc's main path inline when the argument is in
 // its range (integer test on the high word), the full glibc path (early exits, specialcase) out of
@@ -261,9 +262,10 @@ __device__ __noinline__ double photo_miss(const int* target, const float4* ref, 
 // compiler (LFDG_PC_S32 = 2) so that it stays in one register: the generic row pointer was
 // rematerialised from the lane id on every cache probe (8 instructions; refine -3.6 / -1.5 /
 // -3.2 % at C3 / C4 / C5).  0: plain pointer (A/B builds only).
-// LFDG_SKIP_OK: the kFlat 2 gather skips the per-pixel ok test (refine -3.5 / -3.3 % at C3 / C5).
+// LFDG_SKIP_OK: the gather skips the per-pixel ok test — 1: kFlat 2 (refine -3.5 / -3.3 % at C3 /
+// C5), 2: also kFlat 1 / 3 (C4 -3.0 %), 3: also the general kernels (converging rig -3.2 %).
 #ifndef LFDG_SKIP_OK
-#define LFDG_SKIP_OK 1
+#define LFDG_SKIP_OK 3
 #endif
 #ifndef LFDG_PC_S32
 #define LFDG_PC_S32 2
@@ -304,6 +306,12 @@ __device__ __forceinline__ PixGeo pixel_geo(const RefineArgs& a, const double2* 
                 q.sv2 = s;
             }
         }
+    }
+    if (kFlat == 0 && LFDG_SKIP_OK > 2 && !q.ok) q.sv0 = q.sv1 = q.sv2 = __longlong_as_double(0x7ff8000000000000ll);
+    if ((kFlat == 1 || kFlat == 3) && LFDG_SKIP_OK > 1 && !q.ok) {
+        // invisible: z = 1 / z = NaN sends both lrounds of every target to lround_div, which
+        // returns -1 (outside the image) for it, so the gather needs no ok test
+        q.sv2 = q.f_inv = __longlong_as_double(0x7ff8000000000000ll);
     }
     if (kFlat && q.ok) {
         q.f_inv = 1.0 / q.sv2;
@@ -374,7 +382,8 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
                 auto issue = [&](const PixGeo* qq, int4& rr) -> bool {
                     // kFlat == 2: an invisible pixel has f_py = -1, so the bounds test below rejects
                     // it without the ok test (its column is computed from zeros and discarded)
-                    if (!(kFlat == 2 && LFDG_SKIP_OK) && !qq->ok) return false;
+                    // kFlat 1 / 3: its z is NaN, and lround_div returns -1 for it
+                    if (!(LFDG_SKIP_OK > (kFlat == 2 ? 0 : 1)) && !qq->ok) return false;
                     int px, py;
                     const double hx = a.uK00 * (qq->sv0 + T0) + qq->f_kz0;
                     if (!fast_lround_img(hx * qq->f_inv, px)) px = lround_div(hx, qq->sv2);
@@ -433,7 +442,8 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
                 const PixGeo* qp = geo;  // walked as a pointer: a loop-carried register, never recomputed
                 for (int jj = 0; jj < cnt; ++jj, ++qp) {
                     const PixGeo& q = *qp;
-                    if (!q.ok) continue;
+                    // general rigs: an invisible pixel's s v is NaN, so x2 > 0 below rejects it
+                    if (!(LFDG_SKIP_OK > 2) && !q.ok) continue;
                     int px, py;
                     double zt, inv_z;
                     const TargetRow& g = static_cast<const TargetRow*>(w.tg)[t];

@@ -141,3 +141,20 @@ def test_wrong_shapes_raise_before_the_abi():
     with pytest.raises(api.InvalidParams):
         hp.upload(np.zeros((3, 240, 320, 4), np.float32))
     hp.close()
+
+
+def test_views_of_2_31_pixels_rejected_by_the_abi():
+    """Pixel indices are 32-bit: lfdg_set_views rejects a view of 2^31 pixels or more before it
+    reads the images (a one-pixel buffer stands in for them)."""
+    import ctypes as C
+
+    from paper_1812_06856_b200 import _native as N, api
+
+    dc = api.DeviceContext(0)
+    L = N.lib()
+    one = np.zeros(3, np.float32)
+    cams = (N.Camera * 1)()
+    rc = L.lfdg_set_views(dc.h, 1, 1 << 16, 1 << 15, N.ptr(one), C.cast(cams, C.c_void_p), 1.0, 2.0)
+    assert rc == N.LFDG_INVALID_PARAMS
+    assert b"2^31" in L.lfdg_last_error()
+    dc.close()
