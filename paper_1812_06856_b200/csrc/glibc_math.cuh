@@ -240,6 +240,20 @@ __device__ __forceinline__ double exp_nonpos_core_from(double kd, double x) {
     return fma_(scale, tmp, scale);
 }
 __device__ __forceinline__ double exp_nonpos_core(double x) { return exp_nonpos_core_from(exp_nonpos_core_kd(x), x); }
+// the same with the (tail, sbits) table in shared memory (a copy of kExpTabDev)
+__device__ __forceinline__ double exp_nonpos_core_tab(double x, const ulonglong2* tab) {
+    double kd = exp_nonpos_core_kd(x);
+    const uint64_t ki = as_u64(kd);
+    kd = kd - LFDG_EXPC(1);
+    const double r = fma_(kd, LFDG_EXPC(3), fma_(kd, LFDG_EXPC(2), x));
+    const ulonglong2 te = tab[ki & 127u];
+    const double tail = as_f64(te.x);
+    const uint64_t sbits = te.y + (ki << 45);
+    const double r2 = r * r;
+    const double tmp = fma_(r2 * r2, fma_(r, LFDG_EXPC(7), LFDG_EXPC(6)), fma_(fma_(r, LFDG_EXPC(5), LFDG_EXPC(4)), r2, r + tail));
+    const double scale = as_f64(sbits);
+    return fma_(scale, tmp, scale);
+}
 #endif
 
 // __expf_fma (glibc sysdeps/ieee754/flt-32/e_expf.c, x86-64 FMA build).

@@ -110,6 +110,20 @@ __device__ __forceinline__ void accumulate_vis(double& vis_sum, double x) {
         vis_sum += exp_vis_slow(x);
 }
 
+// The linear-rig mode's copy of glibc's exp table in shared memory (LFDG_EXP_SMEM): the table
+// lookup of the visibility exp is one shared load at a link-time address (C3 refine -2.5 %; not
+// for 8-lane candidate slots, where it measured +0.7 % at C5).
+#ifndef LFDG_EXP_SMEM
+#define LFDG_EXP_SMEM 1
+#endif
+__shared__ __align__(16) ulonglong2 s_exptab[128];
+__device__ __forceinline__ void accumulate_vis_smem(double& vis_sum, double x) {
+    if (libm::exp_nonpos_in_core(x))
+        vis_sum += libm::exp_nonpos_core_tab(x, s_exptab);
+    else if (!(x <= -746.0))
+        vis_sum += exp_vis_slow(x);
+}
+
 // depth_consistency (refine.hpp:34-37)
 __device__ __forceinline__ double depth_consistency(double d1, double d2, double two_sigma2) {
     const double r = 1.0 / d1 - 1.0 / d2;
@@ -432,7 +446,10 @@ __device__ __forceinline__ double consistency_pair(const RefineArgs& a, const Wa
                     if (td <= 0) continue;  // no target depth: not in X or Y
                     if (zt <= (double)td * (1.0 + 1e-6)) {
                         const double rr = inv_z - (kFlat == 3 && kRas8 ? 1.0 / (double)td : __hiloint2double(r.w, r.z));
-                        accumulate_vis(vis_sum, -rr * rr * a.inv_two_sigma2);
+                        if (kFlat == 2 && kG != 8 && LFDG_EXP_SMEM)
+                            accumulate_vis_smem(vis_sum, -rr * rr * a.inv_two_sigma2);
+                        else
+                            accumulate_vis(vis_sum, -rr * rr * a.inv_two_sigma2);
                         ++x_count;
                     } else {
                         y_nonempty = true;
@@ -691,6 +708,11 @@ template <bool kIdR, bool kCanonK, int kFlat, bool kRecheck, int kG>
 __global__ void __launch_bounds__(128, refine_min_blocks(kFlat))
     k_refine(RefineArgs a, int n_tasks, int* task_counter, int cap, double4* g_cand, double* g_es, int2* g_acc) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    if constexpr (kFlat == 2 && kG != 8 && LFDG_EXP_SMEM) {
+        for (int i = threadIdx.x; i < 128; i += blockDim.x)
+            s_exptab[i] = reinterpret_cast<const ulonglong2*>(libm::kExpTabDev)[i];
+        __syncthreads();
+    }
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int gwarp = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -1074,9 +1096,10 @@ void refine_iteration(Ctx& c, int l, bool recheck) {
     // four warps per CTA; fewer when the per-warp tables (which grow with the number of matching
     // views) would not fit the 227 KB of shared memory of a CTA — one warp holds ~1000 targets
     const size_t wbytes = warp_smem_bytes(a.N, flat_mode);
-    const int warps = 4 * wbytes <= 227 * 1024 ? 4 : 2 * wbytes <= 227 * 1024 ? 2 : 1;
+    const size_t budget = 227 * 1024 - sizeof(s_exptab);  // less the static exp table
+    const int warps = 4 * wbytes <= budget ? 4 : 2 * wbytes <= budget ? 2 : 1;
     const size_t smem = warps * wbytes;
-    if (smem > 227 * 1024) throw Error(LFDG_INVALID_PARAMS, "too many matching views for the refinement kernel");
+    if (smem > budget) throw Error(LFDG_INVALID_PARAMS, "too many matching views for the refinement kernel");
     if (rn > 0) {
         // the refine gather raster from the current snapshot (labels, depth)
         // many matching views on a non-linear flat rig: the 8-byte raster (kFlat == 3) halves the
